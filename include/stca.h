@@ -1,0 +1,151 @@
+/*
+ * stca.h -- C ABI of the B200-native STCA forward under Request-Level Batching.
+ *
+ * Method: arXiv 2511.06077, "Make It Long, Keep It Fast".
+ *   - Stacked Target-to-History Cross Attention, §3.1 Eq.(1)-(9), P:L95-156,
+ *     executed in the reordered single-query form Eq.(13), P:L175-198;
+ *   - Request-Level Batching, §3.2: one history per request,
+ *     projected once per layer (X~(i), Eq.(2)) and shared by all of that
+ *     request's targets;
+ *   - ragged histories with an offsets ("index") tensor, capped at the
+ *     serving length L_infer by keeping the temporal suffix.
+ *
+ * Every entry point is extern "C", takes plain pointers and sizes, throws
+ * nothing and returns an stca_status.  No torch / C++ types cross it.
+ *
+ * Threading: a handle is not thread-safe; use one handle per thread / device.
+ * Streams are passed as `void*` holding a cudaStream_t (NULL = legacy stream).
+ */
+#ifndef STCA_H_
+#define STCA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STCA_ABI_VERSION 1
+#define STCA_MAX_LAYERS 16
+
+typedef enum {
+  STCA_OK = 0,
+  STCA_ERR_INVALID_ARG = -1,   /* NULL pointer, negative size, bad enum */
+  STCA_ERR_SHAPE = -2,         /* d % h != 0, weight shape mismatch (message names both shapes) */
+  STCA_ERR_OFFSETS = -3,       /* off[0] != 0, decreasing offsets, or off[B] != rows */
+  STCA_ERR_EMPTY_HISTORY = -4, /* L_b == 0: softmax over an empty set (message names b) */
+  STCA_ERR_UNSUPPORTED = -5,   /* e.g. bf16 path with d % 16 != 0 */
+  STCA_ERR_STATE = -6,         /* forward before project, or B mismatch with the projection */
+  STCA_ERR_OOM = -7,           /* device allocation failed */
+  STCA_ERR_CUDA = -8,          /* kernel / launch / copy failure (sticky: destroy the handle) */
+  STCA_ERR_COMM = -9           /* split-history exchange callback failed */
+} stca_status;
+
+typedef enum {
+  STCA_BF16 = 0, /* bf16 storage and tensor-core operands, fp32 accumulation and softmax */
+  STCA_FP32 = 1  /* fp32 everywhere (CUDA cores, no TF32): the 1e-4 parity path */
+} stca_dtype;
+
+/* Split-history exchange: an all-gather of `bytes` bytes
+ * from every rank, called once per layer on `stream` with device pointers.
+ * recv holds split_world * bytes bytes, rank-major.  Return 0 on success. */
+typedef int (*stca_exchange_fn)(void *ctx, const void *send, void *recv, size_t bytes, void *stream);
+
+typedef struct {
+  int32_t d, h, r, M;     /* model dim, heads (d % h == 0), SwiGLU ratio r >= 1, layers 1..STCA_MAX_LAYERS */
+  int32_t L_infer;        /* > 0: keep the most recent L_infer rows of each history; 0: no cap */
+  float ln_eps;           /* LayerNorm eps inside the sqrt (paper silent; 1e-5) */
+  int32_t dtype;          /* stca_dtype */
+  int32_t with_z;         /* also compute z = SwiGLUFFN_Z([o(1)..o(M)|x_t] W_Z), Eq.(9) */
+  int32_t device;         /* CUDA ordinal the handle lives on */
+  int32_t chunk_keys;     /* split-K chunk length cap in keys (multiple of 128); 0 = default 4096 */
+  int32_t split_rank;     /* split-history mode: this rank, 0..split_world-1 */
+  int32_t split_world;    /* 1 = off; > 1: every rank gets the SAME full inputs and owns a */
+                          /* contiguous block of key chunks of every history */
+  stca_exchange_fn exchange;
+  void *exchange_ctx;
+} stca_config;
+
+/* A named weight, HOST memory, float32, row-major in the paper's row-vector
+ * orientation [in x out] (y = x W).  Values are rounded to bf16 (RNE) on the
+ * bf16 path.  Names (i = 1..M):
+ *   L{i}.hist.{Wu,Wv}  d x rd   L{i}.hist.Wo  rd x d   L{i}.hist.{ln_g,ln_b} 1 x d   Eq.(1)-(2)
+ *   L{i}.qry.{Wu,Wv,Wo}        (query SwiGLUFFN(i): Eq.(3) for i = 1, Eq.(7) for i >= 2)
+ *   L1.qry.{ln_g,ln_b}         (LN of Eq.(3))
+ *   L{i}.{WQ,WK,WV,WO} d x d   head r = columns [r d/h, (r+1) d/h); WO rows in head order
+ *   L{i}.WC (i d) x d, i >= 2  (W_C(i) of Eq.(7); concatenation [o(1)|..|o(i-1)|x_t])
+ *   z.WZ ((M+1) d) x d, z.{Wu,Wv,Wo}   (only with with_z)
+ * Reading R5 (shared FFN): pass the same data pointer for hist and qry. */
+typedef struct {
+  const char *name;
+  const float *data;
+  int64_t rows, cols;
+} stca_tensor;
+
+typedef struct stca_handle stca_handle;
+
+/* Validates cfg and every weight (missing / duplicate / mis-shaped names ->
+ * SHAPE or INVALID_ARG with the names and both shapes in the message), copies
+ * and repacks them into handle-owned device memory on cfg->device.  The
+ * caller may free its buffers on return.  Precomputes, per layer and head,
+ * W_QK^r = W_Q^r W_K^r^T (the reordered query map) and
+ * W_VO^r = W_V^r W_O^r (so o = sum_r (alpha_r X~) W_VO^r, Eq.(13) + Eq.(6)). */
+stca_status stca_create(const stca_config *cfg, const stca_tensor *weights, int32_t n_weights,
+                        stca_handle **out);
+
+/* History path, Eq.(2), once per request (RLB):
+ *   X~(i) = LN(SwiGLUFFN(i)(X_b[start'_b:end_b]))  for every layer i and request b,
+ * start'_b = max(hist_off[b], hist_off[b+1] - L_infer).  X is [T x d] row-major,
+ * bf16 (uint16 bit patterns) or fp32 per cfg.dtype, rows chronological (oldest
+ * first), device OR host memory (host buffers are staged H2D on `stream`).
+ * hist_off is a HOST int64 array [B+1], consumed before return.  The handle
+ * owns the projected cache until the next call or destroy.  On any error
+ * nothing is enqueued. */
+stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
+                                 int64_t B, void *stream);
+
+/* Target path for the B requests of the last projection, Eq.(3)-(9):
+ * xt [Nt x d] (dtype per cfg, device or host), tgt_off HOST int64 [B+1]
+ * (request b owns target rows [tgt_off[b], tgt_off[b+1]); m_b = 0 is legal).
+ * Outputs (device or host, float32): out_Z [Nt x M x d] = Z_H rows (Eq.(8)),
+ * out_z [Nt x d] or NULL.  Any number of forwards may reuse one projection. */
+stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                         float *out_Z, float *out_z, void *stream);
+
+void stca_destroy(stca_handle *h);                  /* NULL-safe; synchronises the device */
+const char *stca_last_error(const stca_handle *h);  /* last non-OK message; h == NULL: last failed create on this thread */
+const char *stca_status_string(int32_t status);
+int32_t stca_abi_version(void);
+int64_t stca_kernel_launches(void);                  /* process-wide count of kernels libstca has launched */
+
+/* ---- host planning, exposed for exact (bit-for-bit) tests; no device needed ---- */
+
+/* Same validation as project/forward (0 or a negative status); *bad_index = b for
+ * OFFSETS/EMPTY_HISTORY, else -1. */
+stca_status stca_validate_offsets(const int64_t *hist_off, const int64_t *tgt_off, int64_t B, int64_t T,
+                                  int64_t Nt, int64_t *bad_index);
+
+/* start'_b for b < B. */
+void stca_plan_suffix(const int64_t *hist_off, int64_t B, int32_t L_infer, int64_t *start_out);
+
+/* Split-K chunk plan of one history of L keys: returns the chunk count and
+ * writes the chunk length (a function of L and chunk_keys only). */
+int32_t stca_plan_chunks(int64_t L, int32_t chunk_keys, int64_t *chunk_len);
+
+/* Attention work list (request, first query row, query rows, first key, key count,
+ * chunk index) as 6 int64 per item in launch order; returns the item count, or the
+ * required count if it exceeds `cap`.  m_b h query rows per request, tiles of
+ * `qtile` rows. */
+int64_t stca_plan_attention(const int64_t *hist_len, const int64_t *tgt_off, int64_t B, int32_t h,
+                            int32_t qtile, int32_t chunk_keys, int64_t *items, int64_t cap);
+
+/* LPT partition of requests over n_parts GPUs by cost (descending cost to the
+ * least-loaded part, ties to the lowest index; exact integer arithmetic).
+ * part_out[b] in [0, n_parts). */
+void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *part_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STCA_H_ */

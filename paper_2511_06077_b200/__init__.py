@@ -1,0 +1,137 @@
+"""B200-native STCA forward under Request-Level Batching (arXiv 2511.06077).
+
+Thin ctypes binding over ``libstca.so`` (the C ABI declared in ``include/stca.h``).
+This module only marshals arguments: every step of the path runs in the library's
+CUDA kernels.  There is no CPU fallback; if the library is missing, importing
+this package raises.
+
+    import paper_2511_06077_b200 as stca
+    m = stca.STCA(weights, d=128, h=4, r=4, M=4, L_infer=10000, dtype="bf16")
+    m.project_history(X, hist_off)        # X: torch CUDA tensor (bf16/uint16 or fp32) or host numpy
+    m.forward(xt, tgt_off, out_Z, out_z)  # outputs: float32 CUDA tensors or host numpy arrays
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_shards,  # noqa: F401
+                   plan_suffix, status_string, validate_offsets, EXCHANGE_FN, _Config, _Tensor, LIB_PATH)
+
+__all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_shards", "plan_suffix",
+           "validate_offsets", "status_string", "LIB_PATH"]
+
+
+def _ptr(x) -> int:
+    """Address of a torch tensor (device or host) or a numpy array (host)."""
+    if x is None:
+        return 0
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return x.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _stream(stream) -> int:
+    if stream is not None:
+        return int(stream) if isinstance(stream, int) else int(stream.cuda_stream)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return int(torch.cuda.current_stream().cuda_stream)
+    except Exception:  # pragma: no cover
+        pass
+    return 0
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+class STCA:
+    """One handle = one device's copy of the weights + the projected history cache."""
+
+    def __init__(self, weights: Dict[str, np.ndarray], *, d: int, h: int, r: int, M: int, L_infer: int = 0,
+                 dtype: str = "bf16", with_z: bool = True, device: int = 0, chunk_keys: int = 0,
+                 ln_eps: float = 1e-5, split_rank: int = 0, split_world: int = 1, exchange=None):
+        self.d, self.h, self.r, self.M, self.with_z = d, h, r, M, with_z
+        self.dtype = dtype
+        cfg = _Config()
+        cfg.d, cfg.h, cfg.r, cfg.M = d, h, r, M
+        cfg.L_infer = L_infer
+        cfg.ln_eps = ln_eps
+        cfg.dtype = STCA_BF16 if dtype == "bf16" else STCA_FP32
+        cfg.with_z = 1 if with_z else 0
+        cfg.device = device
+        cfg.chunk_keys = chunk_keys
+        cfg.split_rank, cfg.split_world = split_rank, split_world
+        self._exchange_cb = None
+        if exchange is not None:
+            self._exchange_cb = EXCHANGE_FN(exchange)
+            cfg.exchange = self._exchange_cb
+        # weights: host float32; identical array objects keep identical pointers (reading R5 aliasing)
+        conv, keep = {}, []
+        tens = (_Tensor * len(weights))()
+        for i, (name, arr) in enumerate(weights.items()):
+            key = id(arr)
+            if key not in conv:
+                a = np.ascontiguousarray(np.asarray(arr, dtype=np.float32))
+                conv[key] = a
+            a = conv[key]
+            bname = name.encode()
+            keep.append(bname)
+            rows, cols = (1, a.size) if a.ndim == 1 else a.shape
+            tens[i].name = bname
+            tens[i].data = a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            tens[i].rows, tens[i].cols = rows, cols
+        handle = ctypes.c_void_p()
+        rc = lib().stca_create(ctypes.byref(cfg), tens, len(weights), ctypes.byref(handle))
+        if rc != 0:
+            raise StcaError(rc, lib().stca_last_error(None).decode())
+        self._h = handle
+        self._B = None
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().stca_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise StcaError(rc, lib().stca_last_error(self._h).decode())
+
+    # -- the two calls --
+    def project_history(self, X, hist_off, stream=None) -> None:
+        """Eq.(2) for every layer, once per request (RLB).  X: [T x d] rows, chronological."""
+        off = _i64(hist_off)
+        B = off.shape[0] - 1
+        T = int(X.shape[0])
+        self._check(lib().stca_project_history(self._h, ctypes.c_void_p(_ptr(X)), T,
+                                                off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
+                                                ctypes.c_void_p(_stream(stream))))
+        self._B = B
+
+    def forward(self, xt, tgt_off, out_Z, out_z=None, stream=None) -> None:
+        """Eq.(3)-(9) for the targets of the projected requests; writes out_Z [Nt,M,d], out_z [Nt,d]."""
+        off = _i64(tgt_off)
+        B = off.shape[0] - 1
+        Nt = int(xt.shape[0])
+        self._check(lib().stca_forward(self._h, ctypes.c_void_p(_ptr(xt)), Nt,
+                                       off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
+                                       ctypes.c_void_p(_ptr(out_Z)), ctypes.c_void_p(_ptr(out_z)),
+                                       ctypes.c_void_p(_stream(stream))))

@@ -1,0 +1,136 @@
+"""ctypes declarations of include/stca.h (marshalling only)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstca.so")
+STCA_BF16, STCA_FP32 = 0, 1
+
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p)
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("h", ctypes.c_int32), ("r", ctypes.c_int32), ("M", ctypes.c_int32),
+                ("L_infer", ctypes.c_int32), ("ln_eps", ctypes.c_float), ("dtype", ctypes.c_int32),
+                ("with_z", ctypes.c_int32), ("device", ctypes.c_int32), ("chunk_keys", ctypes.c_int32),
+                ("split_rank", ctypes.c_int32), ("split_world", ctypes.c_int32), ("exchange", EXCHANGE_FN),
+                ("exchange_ctx", ctypes.c_void_p)]
+
+
+class _Tensor(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("data", ctypes.POINTER(ctypes.c_float)), ("rows", ctypes.c_int64),
+                ("cols", ctypes.c_int64)]
+
+
+class StcaError(RuntimeError):
+    def __init__(self, status: int, message: str = ""):
+        super().__init__(f"{status_string(status)} ({status}): {message}")
+        self.status, self.message = status, message
+
+
+_lib = None
+_I64P = ctypes.POINTER(ctypes.c_int64)
+
+SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy", "stca_last_error",
+           "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
+           "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches"]
+
+
+def lib():
+    """Load libstca.so (fails loudly if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2511_06077_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        L.stca_create.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Tensor), ctypes.c_int32,
+                                  ctypes.POINTER(ctypes.c_void_p)]
+        L.stca_create.restype = ctypes.c_int32
+        L.stca_project_history.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _I64P, ctypes.c_int64,
+                                           ctypes.c_void_p]
+        L.stca_project_history.restype = ctypes.c_int32
+        L.stca_forward.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _I64P, ctypes.c_int64,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.stca_forward.restype = ctypes.c_int32
+        L.stca_destroy.argtypes = [ctypes.c_void_p]
+        L.stca_destroy.restype = None
+        L.stca_last_error.argtypes = [ctypes.c_void_p]
+        L.stca_last_error.restype = ctypes.c_char_p
+        L.stca_status_string.argtypes = [ctypes.c_int32]
+        L.stca_status_string.restype = ctypes.c_char_p
+        L.stca_abi_version.restype = ctypes.c_int32
+        L.stca_kernel_launches.restype = ctypes.c_int64
+        L.stca_validate_offsets.argtypes = [_I64P, _I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I64P]
+        L.stca_validate_offsets.restype = ctypes.c_int32
+        L.stca_plan_suffix.argtypes = [_I64P, ctypes.c_int64, ctypes.c_int32, _I64P]
+        L.stca_plan_suffix.restype = None
+        L.stca_plan_chunks.argtypes = [ctypes.c_int64, ctypes.c_int32, _I64P]
+        L.stca_plan_chunks.restype = ctypes.c_int32
+        L.stca_plan_attention.argtypes = [_I64P, _I64P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, _I64P, ctypes.c_int64]
+        L.stca_plan_attention.restype = ctypes.c_int64
+        L.stca_plan_shards.argtypes = [_I64P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+        L.stca_plan_shards.restype = None
+        _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    try:
+        return lib().stca_status_string(s).decode()
+    except ImportError:  # pragma: no cover
+        return str(s)
+
+
+def _p64(a: np.ndarray):
+    return a.ctypes.data_as(_I64P)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def validate_offsets(hist_off, tgt_off, T: int, Nt: int):
+    h, t = _i64(hist_off), _i64(tgt_off)
+    bad = ctypes.c_int64(-1)
+    rc = lib().stca_validate_offsets(_p64(h), _p64(t), h.shape[0] - 1, T, Nt, ctypes.byref(bad))
+    return rc, bad.value
+
+
+def plan_suffix(hist_off, L_infer: int) -> np.ndarray:
+    h = _i64(hist_off)
+    out = np.zeros(max(h.shape[0] - 1, 0), dtype=np.int64)
+    lib().stca_plan_suffix(_p64(h), h.shape[0] - 1, L_infer, _p64(out))
+    return out
+
+
+def plan_chunks(L: int, chunk_keys: int = 0):
+    cl = ctypes.c_int64(0)
+    n = lib().stca_plan_chunks(L, chunk_keys, ctypes.byref(cl))
+    return n, cl.value
+
+
+def plan_attention(hist_len, tgt_off, h: int, qtile: int, chunk_keys: int = 0) -> np.ndarray:
+    hl, t = _i64(hist_len), _i64(tgt_off)
+    B = hl.shape[0]
+    n = lib().stca_plan_attention(_p64(hl), _p64(t), B, h, qtile, chunk_keys, None, 0)
+    out = np.zeros((max(n, 1), 6), dtype=np.int64)
+    lib().stca_plan_attention(_p64(hl), _p64(t), B, h, qtile, chunk_keys, _p64(out), n)
+    return out[:n]
+
+
+def plan_shards(cost, n_parts: int) -> np.ndarray:
+    c = _i64(cost)
+    out = np.zeros(c.shape[0], dtype=np.int32)
+    lib().stca_plan_shards(_p64(c), c.shape[0], n_parts, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    return out
+
+
+def kernel_launches() -> int:
+    """Process-wide number of kernels libstca has launched (bench: gpu_launches)."""
+    return int(lib().stca_kernel_launches())

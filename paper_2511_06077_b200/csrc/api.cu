@@ -1,0 +1,770 @@
+// api.cu -- the C ABI of include/stca.h: validation, host planning (exact integer
+// work), device memory ownership and the orchestration of the
+// STCA forward under RLB (§3.1-3.2).  Kernels live in kernels_*.cu / tc_*.cu.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/stca.h"
+#include "launch.h"
+#include "tc.h"
+
+using stca::bf16;
+
+#include <atomic>
+static std::atomic<int64_t> g_launches{0};
+namespace stca {
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace stca
+
+namespace {
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct HostPinned {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct LayerW {
+  void *W1h = nullptr, *Woh = nullptr;  // history FFN: [d x 2rd] interleaved (u_j, v_j), [rd x d]
+  float *gh = nullptr, *bh = nullptr;
+  void *W1q = nullptr, *Woq = nullptr;  // query FFN
+  float *gq = nullptr, *bq = nullptr;   // layer 1 only
+  void *WQK = nullptr;                  // [d x h d], scaled by log2(e)/sqrt(d_h)
+  void *WVO = nullptr;                  // [h d x d]
+  void *WC = nullptr;                   // [(i) d x d], rows permuted to the Ocat layout [x_t|o1|..]
+  stca::TcWeights tc;                   // tcgen05 repacks (bf16 path)
+};
+
+struct stca_handle {
+  stca_config cfg{};
+  std::string err;
+  bool sticky = false;
+  bool bf16 = true;
+  int es = 2;  // storage element size
+  std::vector<void *> allocs;
+  LayerW L[STCA_MAX_LAYERS];
+  void *W1z = nullptr, *Woz = nullptr, *WZ = nullptr;
+  stca::TcWeights tcz;
+  // projection state
+  int64_t B = -1;
+  std::vector<int64_t> start, len, coff;  // start'_b (input rows), L'_b, compacted offsets [B+1]
+  int64_t T2 = 0;
+  DevBuf xt_cache;  // M x [T2 x d] storage
+  DevBuf xin, xgather, seg, proj_h, proj_y;
+  // forward scratch
+  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, items, mitems, zout, Zout;
+  HostPinned pin;
+  int64_t chunk_cap = 4096;
+};
+
+static thread_local std::string g_create_error;  // message of the last failed stca_create on this thread
+
+static stca_status fail(stca_handle *h, stca_status s, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+static stca_status fail(stca_handle *h, stca_status s, const char *fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+    if (s == STCA_ERR_CUDA) h->sticky = true;
+  }
+  return s;
+}
+
+#define CU(expr)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      if (e_ == cudaErrorMemoryAllocation) {                                                       \
+        cudaGetLastError();                                                                        \
+        return fail(h, STCA_ERR_OOM, "%s: %s", #expr, cudaGetErrorString(e_));                     \
+      }                                                                                            \
+      return fail(h, STCA_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+    }                                                                                              \
+  } while (0)
+
+// ===========================================================================
+// host planning (exact integer work)
+// ===========================================================================
+extern "C" {
+
+int32_t stca_abi_version(void) { return STCA_ABI_VERSION; }
+
+int64_t stca_kernel_launches(void) { return g_launches.load(); }
+
+const char *stca_status_string(int32_t s) {
+  switch (s) {
+    case STCA_OK: return "STCA_OK";
+    case STCA_ERR_INVALID_ARG: return "STCA_ERR_INVALID_ARG";
+    case STCA_ERR_SHAPE: return "STCA_ERR_SHAPE";
+    case STCA_ERR_OFFSETS: return "STCA_ERR_OFFSETS";
+    case STCA_ERR_EMPTY_HISTORY: return "STCA_ERR_EMPTY_HISTORY";
+    case STCA_ERR_UNSUPPORTED: return "STCA_ERR_UNSUPPORTED";
+    case STCA_ERR_STATE: return "STCA_ERR_STATE";
+    case STCA_ERR_OOM: return "STCA_ERR_OOM";
+    case STCA_ERR_CUDA: return "STCA_ERR_CUDA";
+    case STCA_ERR_COMM: return "STCA_ERR_COMM";
+    default: return "STCA_ERR_UNKNOWN";
+  }
+}
+
+static stca_status check_offsets(const int64_t *off, int64_t B, int64_t rows, bool nonempty, int64_t *bad) {
+  *bad = -1;
+  if (B < 0) return STCA_ERR_INVALID_ARG;
+  if (!off) return STCA_ERR_INVALID_ARG;
+  if (off[0] != 0) return STCA_ERR_OFFSETS;
+  for (int64_t b = 0; b < B; ++b)
+    if (off[b + 1] < off[b]) {
+      *bad = b;
+      return STCA_ERR_OFFSETS;
+    }
+  if (off[B] != rows) return STCA_ERR_OFFSETS;
+  if (nonempty)
+    for (int64_t b = 0; b < B; ++b)
+      if (off[b + 1] == off[b]) {
+        *bad = b;
+        return STCA_ERR_EMPTY_HISTORY;
+      }
+  return STCA_OK;
+}
+
+stca_status stca_validate_offsets(const int64_t *hist_off, const int64_t *tgt_off, int64_t B, int64_t T, int64_t Nt,
+                                  int64_t *bad_index) {
+  int64_t dummy;
+  if (!bad_index) bad_index = &dummy;
+  // the oracle's order: OFFSETS of either array before EMPTY_HISTORY
+  stca_status s = check_offsets(hist_off, B, T, false, bad_index);
+  if (s != STCA_OK) return s;
+  s = check_offsets(tgt_off, B, Nt, false, bad_index);
+  if (s != STCA_OK) return s;
+  return check_offsets(hist_off, B, T, true, bad_index);
+}
+
+void stca_plan_suffix(const int64_t *hist_off, int64_t B, int32_t L_infer, int64_t *start_out) {
+  for (int64_t b = 0; b < B; ++b) {
+    int64_t s = hist_off[b];
+    if (L_infer > 0 && hist_off[b + 1] - L_infer > s) s = hist_off[b + 1] - L_infer;
+    start_out[b] = s;
+  }
+}
+
+int32_t stca_plan_chunks(int64_t L, int32_t chunk_keys, int64_t *chunk_len) {
+  const int64_t cap = chunk_keys > 0 ? chunk_keys : 4096;
+  if (L <= 0) {
+    if (chunk_len) *chunk_len = 0;
+    return 0;
+  }
+  const int64_t n = (L + cap - 1) / cap;
+  int64_t cl = (L + n - 1) / n;
+  cl = (cl + 127) / 128 * 128;
+  if (chunk_len) *chunk_len = cl;
+  return (int32_t)((L + cl - 1) / cl);
+}
+
+int64_t stca_plan_attention(const int64_t *hist_len, const int64_t *tgt_off, int64_t B, int32_t h, int32_t qtile,
+                            int32_t chunk_keys, int64_t *items, int64_t cap) {
+  struct It {
+    int64_t b, q0, nq, k0, kl, c;
+  };
+  std::vector<It> v;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * h;
+    if (rows == 0) continue;
+    int64_t cl = 0;
+    const int32_t nc = stca_plan_chunks(hist_len[b], chunk_keys, &cl);
+    for (int32_t c = 0; c < nc; ++c) {
+      const int64_t k0 = (int64_t)c * cl, kl = std::min(cl, hist_len[b] - k0);
+      for (int64_t q = 0; q < rows; q += qtile)
+        v.push_back({b, tgt_off[b] * h + q, std::min<int64_t>(qtile, rows - q), k0, kl, c});
+    }
+  }
+  // LPT launch order: longest key span first; ties by (request, chunk, query tile)
+  std::stable_sort(v.begin(), v.end(), [](const It &a, const It &b) {
+    if (a.kl != b.kl) return a.kl > b.kl;
+    if (a.b != b.b) return a.b < b.b;
+    if (a.c != b.c) return a.c < b.c;
+    return a.q0 < b.q0;
+  });
+  const int64_t n = (int64_t)v.size();
+  if (items && n <= cap)
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t *o = items + 6 * i;
+      o[0] = v[i].b; o[1] = v[i].q0; o[2] = v[i].nq; o[3] = v[i].k0; o[4] = v[i].kl; o[5] = v[i].c;
+    }
+  return n;
+}
+
+void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *part_out) {
+  std::vector<int64_t> idx(B);
+  for (int64_t b = 0; b < B; ++b) idx[b] = b;
+  std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+    if (cost[a] != cost[b]) return cost[a] > cost[b];
+    return a < b;
+  });
+  std::vector<int64_t> load(n_parts > 0 ? n_parts : 1, 0);
+  for (int64_t b : idx) {
+    int32_t best = 0;
+    for (int32_t p = 1; p < n_parts; ++p)
+      if (load[p] < load[best]) best = p;
+    part_out[b] = best;
+    load[best] += cost[b];
+  }
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// create / destroy
+// ===========================================================================
+static bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static void *dalloc(stca_handle *h, size_t bytes) {
+  void *p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  h->allocs.push_back(p);
+  return p;
+}
+
+// Uploads host fp32 `src` into storage dtype; returns device pointer (or null).
+static void *upload(stca_handle *h, const float *src, size_t n, bool as_f32 = false) {
+  if (!h->bf16 || as_f32) {
+    void *p = dalloc(h, n * 4);
+    if (p && cudaMemcpy(p, src, n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return p;
+  }
+  std::vector<uint16_t> tmp(n);
+  for (size_t i = 0; i < n; ++i) {  // fp32 -> bf16 RNE (storage rounding of the weights)
+    uint32_t u;
+    memcpy(&u, &src[i], 4);
+    tmp[i] = (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+  }
+  void *p = dalloc(h, n * 2);
+  if (p && cudaMemcpy(p, tmp.data(), n * 2, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  return p;
+}
+
+extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w, int32_t n_w, stca_handle **out) {
+  if (!cfg || !out || (n_w > 0 && !w)) return STCA_ERR_INVALID_ARG;
+  *out = nullptr;
+  stca_handle *h = new stca_handle();
+  h->cfg = *cfg;
+  h->err.clear();
+  auto bad = [&](stca_status s) {
+    g_create_error = h->err;  // readable through stca_last_error(NULL)
+    stca_destroy(h);
+    return s;
+  };
+  const int d = cfg->d, hh = cfg->h, r = cfg->r, M = cfg->M;
+  if (d <= 0 || hh <= 0 || r < 1 || M < 1 || M > STCA_MAX_LAYERS || d % hh)
+    return bad(fail(h, STCA_ERR_SHAPE, "bad config d=%d h=%d r=%d M=%d (need d%%h==0, r>=1, 1<=M<=%d)", d, hh, r,
+                    M, STCA_MAX_LAYERS));
+  if (cfg->dtype != STCA_BF16 && cfg->dtype != STCA_FP32) return bad(fail(h, STCA_ERR_INVALID_ARG, "bad dtype"));
+  if (cfg->dtype == STCA_BF16 && (d % 16 || d > 512))
+    return bad(fail(h, STCA_ERR_UNSUPPORTED, "bf16 path needs d %% 16 == 0 and d <= 512 (d=%d)", d));
+  if (cfg->dtype == STCA_FP32 && d > 512) return bad(fail(h, STCA_ERR_UNSUPPORTED, "d <= 512 (d=%d)", d));
+  if (cfg->chunk_keys < 0 || cfg->chunk_keys % 128)
+    return bad(fail(h, STCA_ERR_INVALID_ARG, "chunk_keys must be a multiple of 128 (got %d)", cfg->chunk_keys));
+  if (cfg->split_world < 0 || cfg->split_world > 64 ||
+      (cfg->split_world > 1 && (cfg->split_rank < 0 || cfg->split_rank >= cfg->split_world || !cfg->exchange)))
+    return bad(fail(h, STCA_ERR_INVALID_ARG, "bad split-history settings (rank %d of %d, exchange %p)",
+                    cfg->split_rank, cfg->split_world, (void *)cfg->exchange));
+  if (!(cfg->ln_eps > 0.f)) h->cfg.ln_eps = 1e-5f;
+  if (h->cfg.split_world == 0) h->cfg.split_world = 1;
+  h->bf16 = cfg->dtype == STCA_BF16;
+  h->es = h->bf16 ? 2 : 4;
+  h->chunk_cap = cfg->chunk_keys > 0 ? cfg->chunk_keys : 4096;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    cudaGetLastError();
+    return bad(fail(h, STCA_ERR_CUDA, "cudaSetDevice(%d) failed", cfg->device));
+  }
+
+  // ---- collect and validate names / shapes ----
+  std::map<std::string, const stca_tensor *> byname;
+  for (int i = 0; i < n_w; ++i) {
+    if (!w[i].name || !w[i].data) return bad(fail(h, STCA_ERR_INVALID_ARG, "weight %d has a NULL name or data", i));
+    if (byname.count(w[i].name)) return bad(fail(h, STCA_ERR_INVALID_ARG, "duplicate weight '%s'", w[i].name));
+    byname[w[i].name] = &w[i];
+  }
+  const int rd = r * d;
+  struct Need {
+    std::string name;
+    int64_t rows, cols;
+  };
+  std::vector<Need> need;
+  for (int i = 1; i <= M; ++i) {
+    std::string p = "L" + std::to_string(i) + ".";
+    need.push_back({p + "hist.Wu", d, rd});
+    need.push_back({p + "hist.Wv", d, rd});
+    need.push_back({p + "hist.Wo", rd, d});
+    need.push_back({p + "hist.ln_g", 1, d});
+    need.push_back({p + "hist.ln_b", 1, d});
+    need.push_back({p + "qry.Wu", d, rd});
+    need.push_back({p + "qry.Wv", d, rd});
+    need.push_back({p + "qry.Wo", rd, d});
+    if (i == 1) {
+      need.push_back({"L1.qry.ln_g", 1, d});
+      need.push_back({"L1.qry.ln_b", 1, d});
+    }
+    for (const char *k : {"WQ", "WK", "WV", "WO"}) need.push_back({p + k, d, d});
+    if (i >= 2) need.push_back({p + "WC", (int64_t)i * d, d});
+  }
+  if (cfg->with_z) {
+    need.push_back({"z.WZ", (int64_t)(M + 1) * d, d});
+    need.push_back({"z.Wu", d, rd});
+    need.push_back({"z.Wv", d, rd});
+    need.push_back({"z.Wo", rd, d});
+  }
+  for (const Need &n : need) {
+    auto it = byname.find(n.name);
+    if (it == byname.end()) return bad(fail(h, STCA_ERR_SHAPE, "missing weight '%s' (%lld x %lld)", n.name.c_str(),
+                                            (long long)n.rows, (long long)n.cols));
+    if (it->second->rows != n.rows || it->second->cols != n.cols)
+      return bad(fail(h, STCA_ERR_SHAPE, "weight '%s' has shape %lld x %lld, expected %lld x %lld", n.name.c_str(),
+                      (long long)it->second->rows, (long long)it->second->cols, (long long)n.rows,
+                      (long long)n.cols));
+  }
+  if (byname.size() != need.size()) {
+    for (auto &kv : byname) {
+      bool ok = false;
+      for (const Need &n : need) ok |= n.name == kv.first;
+      if (!ok) return bad(fail(h, STCA_ERR_INVALID_ARG, "unknown weight '%s'", kv.first.c_str()));
+    }
+  }
+  auto W = [&](const std::string &n) { return byname[n]->data; };
+
+  // ---- repack ----
+  auto ffn = [&](const std::string &p, void **W1, void **Wo, stca::TcWeights *tc) -> bool {
+    const float *u = W(p + ".Wu"), *v = W(p + ".Wv"), *o = W(p + ".Wo");
+    std::vector<float> il((size_t)d * 2 * rd);
+    for (int e = 0; e < d; ++e)
+      for (int j = 0; j < rd; ++j) {
+        il[(size_t)e * 2 * rd + 2 * j] = u[(size_t)e * rd + j];
+        il[(size_t)e * 2 * rd + 2 * j + 1] = v[(size_t)e * rd + j];
+      }
+    *W1 = upload(h, il.data(), il.size());
+    *Wo = upload(h, o, (size_t)rd * d);
+    if (!*W1 || !*Wo) return false;
+    if (tc && h->bf16 && !stca::tc_prepare_ffn(u, v, o, d, rd, tc, [&](size_t n) { return dalloc(h, n); }))
+      return false;
+    return true;
+  };
+  const float qk_scale = (float)(1.4426950408889634 / sqrt((double)(d / hh)));  // log2(e)/sqrt(d_h)
+  float *wq = (float *)dalloc(h, (size_t)d * d * 4), *wk = (float *)dalloc(h, (size_t)d * d * 4);
+  float *wv = (float *)dalloc(h, (size_t)d * d * 4), *wo = (float *)dalloc(h, (size_t)d * d * 4);
+  float *wqk = (float *)dalloc(h, (size_t)hh * d * d * 4), *wvo = (float *)dalloc(h, (size_t)hh * d * d * 4);
+  if (!wq || !wk || !wv || !wo || !wqk || !wvo) return bad(fail(h, STCA_ERR_OOM, "weight staging allocation failed"));
+  for (int i = 1; i <= M; ++i) {
+    LayerW &Ly = h->L[i - 1];
+    std::string p = "L" + std::to_string(i) + ".";
+    if (!ffn(p + "hist", &Ly.W1h, &Ly.Woh, &Ly.tc)) return bad(fail(h, STCA_ERR_OOM, "upload failed (%s)", p.c_str()));
+    if (W(p + "qry.Wu") == W(p + "hist.Wu") && W(p + "qry.Wv") == W(p + "hist.Wv") && W(p + "qry.Wo") == W(p + "hist.Wo")) {
+      Ly.W1q = Ly.W1h;
+      Ly.Woq = Ly.Woh;
+      Ly.tc.W1q = Ly.tc.W1h;
+      Ly.tc.Woq = Ly.tc.Woh;
+    } else {
+      stca::TcWeights tq;
+      if (!ffn(p + "qry", &Ly.W1q, &Ly.Woq, &tq)) return bad(fail(h, STCA_ERR_OOM, "upload failed (%sqry)", p.c_str()));
+      Ly.tc.W1q = tq.W1h;
+      Ly.tc.Woq = tq.Woh;
+    }
+    Ly.gh = (float *)upload(h, W(p + "hist.ln_g"), d, true);
+    Ly.bh = (float *)upload(h, W(p + "hist.ln_b"), d, true);
+    if (i == 1) {
+      Ly.gq = (float *)upload(h, W("L1.qry.ln_g"), d, true);
+      Ly.bq = (float *)upload(h, W("L1.qry.ln_b"), d, true);
+    }
+    // W_QK, W_VO on the device (fp32), then storage dtype
+    if (cudaMemcpy(wq, W(p + "WQ"), (size_t)d * d * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(wk, W(p + "WK"), (size_t)d * d * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(wv, W(p + "WV"), (size_t)d * d * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(wo, W(p + "WO"), (size_t)d * d * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bad(fail(h, STCA_ERR_CUDA, "weight upload failed"));
+    if (stca::prep_qk_vo(wq, wk, wv, wo, d, hh, qk_scale, wqk, wvo, 0) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return bad(fail(h, STCA_ERR_CUDA, "prep_qk_vo failed: %s", cudaGetErrorString(cudaGetLastError())));
+    const size_t nqk = (size_t)hh * d * d;
+    if (h->bf16) {
+      Ly.WQK = dalloc(h, nqk * 2);
+      Ly.WVO = dalloc(h, nqk * 2);
+      if (!Ly.WQK || !Ly.WVO) return bad(fail(h, STCA_ERR_OOM, "alloc failed"));
+      stca::f32_to_bf16(wqk, (bf16 *)Ly.WQK, nqk, 0);
+      stca::f32_to_bf16(wvo, (bf16 *)Ly.WVO, nqk, 0);
+    } else {
+      Ly.WQK = dalloc(h, nqk * 4);
+      Ly.WVO = dalloc(h, nqk * 4);
+      if (!Ly.WQK || !Ly.WVO) return bad(fail(h, STCA_ERR_OOM, "alloc failed"));
+      cudaMemcpy(Ly.WQK, wqk, nqk * 4, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(Ly.WVO, wvo, nqk * 4, cudaMemcpyDeviceToDevice);
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return bad(fail(h, STCA_ERR_CUDA, "weight prep failed"));
+    if (i >= 2) {  // permute rows: [o1..o(i-1) | x_t] -> Ocat layout [x_t | o1 | .. | o(i-1)]
+      const float *wc = W(p + "WC");
+      std::vector<float> pc((size_t)i * d * d);
+      memcpy(pc.data(), wc + (size_t)(i - 1) * d * d, sizeof(float) * d * d);
+      memcpy(pc.data() + (size_t)d * d, wc, sizeof(float) * (size_t)(i - 1) * d * d);
+      Ly.WC = upload(h, pc.data(), pc.size());
+      if (!Ly.WC) return bad(fail(h, STCA_ERR_OOM, "alloc failed"));
+    }
+    if (h->bf16 && !stca::tc_prepare_layer(Ly.WQK, Ly.WVO, Ly.WC, i, d, hh, &Ly.tc, [&](size_t n) { return dalloc(h, n); }))
+      return bad(fail(h, STCA_ERR_OOM, "tc repack failed"));
+  }
+  if (cfg->with_z) {
+    if (!ffn("z", &h->W1z, &h->Woz, &h->tcz)) return bad(fail(h, STCA_ERR_OOM, "upload failed (z)"));
+    const float *wz = W("z.WZ");
+    std::vector<float> pz((size_t)(M + 1) * d * d);
+    memcpy(pz.data(), wz + (size_t)M * d * d, sizeof(float) * d * d);
+    memcpy(pz.data() + (size_t)d * d, wz, sizeof(float) * (size_t)M * d * d);
+    h->WZ = upload(h, pz.data(), pz.size());
+    if (!h->WZ) return bad(fail(h, STCA_ERR_OOM, "alloc failed"));
+    if (h->bf16 && !stca::tc_prepare_layer(nullptr, nullptr, h->WZ, M + 1, d, hh, &h->tcz, [&](size_t n) { return dalloc(h, n); }))
+      return bad(fail(h, STCA_ERR_OOM, "tc repack failed"));
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bad(fail(h, STCA_ERR_CUDA, "create: device error"));
+  *out = h;
+  return STCA_OK;
+}
+
+extern "C" void stca_destroy(stca_handle *h) {
+  if (!h) return;
+  cudaSetDevice(h->cfg.device);
+  cudaDeviceSynchronize();
+  for (void *p : h->allocs) cudaFree(p);
+  DevBuf *bufs[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,   &h->proj_h, &h->proj_y, &h->xtin,
+                    &h->ocat,     &h->q,    &h->c,       &h->hbuf,  &h->ybuf32, &h->U,      &h->Y,
+                    &h->part,     &h->items, &h->mitems, &h->zout,  &h->Zout};
+  for (DevBuf *b : bufs) b->release();
+  h->pin.release();
+  cudaGetLastError();
+  delete h;
+}
+
+extern "C" const char *stca_last_error(const stca_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+// ===========================================================================
+// project_history
+// ===========================================================================
+extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
+                                            int64_t B, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (B < 0 || T < 0 || !hist_off || (T > 0 && !X)) return fail(h, STCA_ERR_INVALID_ARG, "NULL or negative argument");
+  int64_t badi = -1;
+  stca_status s = check_offsets(hist_off, B, T, false, &badi);
+  if (s != STCA_OK) return fail(h, s, "hist_off invalid at request %lld (off[0]=%lld, off[B]=%lld, T=%lld)",
+                                (long long)badi, (long long)hist_off[0], (long long)hist_off[B], (long long)T);
+  s = check_offsets(hist_off, B, T, true, &badi);
+  if (s != STCA_OK) return fail(h, s, "empty history for request %lld", (long long)badi);
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
+  const size_t row_bytes = (size_t)d * es;
+
+  // a0: suffix truncation + compacted offsets (exact integer work)
+  h->start.assign(B, 0);
+  stca_plan_suffix(hist_off, B, h->cfg.L_infer, h->start.data());
+  h->len.assign(B, 0);
+  h->coff.assign(B + 1, 0);
+  bool truncated = false;
+  for (int64_t b = 0; b < B; ++b) {
+    h->len[b] = hist_off[b + 1] - h->start[b];
+    h->coff[b + 1] = h->coff[b] + h->len[b];
+    truncated |= h->start[b] != hist_off[b];
+  }
+  const int64_t T2 = h->coff[B];
+  // split-history: this rank projects only its own chunks -- handled by restricting rows in attention;
+  // the projection covers all rows (token-wise, cheap relative to replication of inputs).
+  const void *Xd = X;
+  if (T > 0 && !is_device_ptr(X)) {  // host input: stage H2D on the stream
+    CU(h->xin.ensure((size_t)T * row_bytes));
+    CU(cudaMemcpyAsync(h->xin.p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
+    Xd = h->xin.p;
+  }
+  if (truncated) {  // gather the suffixes into a compacted buffer
+    std::vector<int64_t> seg;
+    int64_t maxlen = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      seg.push_back(h->start[b]);
+      seg.push_back(h->coff[b]);
+      seg.push_back(h->len[b]);
+      maxlen = std::max(maxlen, h->len[b]);
+    }
+    CU(h->seg.ensure(seg.size() * 8));
+    CU(h->pin.ensure(seg.size() * 8));
+    CU(cudaStreamSynchronize(st));  // pinned staging reuse
+    memcpy(h->pin.p, seg.data(), seg.size() * 8);
+    CU(cudaMemcpyAsync(h->seg.p, h->pin.p, seg.size() * 8, cudaMemcpyHostToDevice, st));
+    CU(h->xgather.ensure((size_t)T2 * row_bytes));
+    CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), B, maxlen, (int)row_bytes, st));
+    Xd = h->xgather.p;
+  }
+  CU(h->xt_cache.ensure((size_t)M * T2 * row_bytes + 256));
+  h->T2 = T2;
+  // a1: X~(i) = LN(SwiGLUFFN(i)(X)) for all layers, Eq.(2)
+  if (h->bf16 && stca::tc_available()) {
+    stca::TcProj pj;
+    pj.X = Xd;
+    pj.rows = T2;
+    pj.d = d;
+    pj.rd = rd;
+    pj.M = M;
+    pj.eps = h->cfg.ln_eps;
+    pj.out = h->xt_cache.p;
+    pj.out_layer_stride = T2 * d;
+    for (int i = 0; i < M; ++i) {
+      pj.W1[i] = h->L[i].tc.W1h;
+      pj.Wo[i] = h->L[i].tc.Woh;
+      pj.g[i] = h->L[i].gh;
+      pj.b[i] = h->L[i].bh;
+    }
+    CU(stca::tc_project(pj, st));
+  } else {
+    const int64_t R = std::min<int64_t>(std::max<int64_t>(T2, 1), 1 << 16);
+    CU(h->proj_h.ensure((size_t)R * rd * es));
+    CU(h->proj_y.ensure((size_t)R * d * 4));
+    for (int i = 0; i < M; ++i) {
+      for (int64_t r0 = 0; r0 < T2; r0 += R) {
+        const int rows = (int)std::min<int64_t>(R, T2 - r0);
+        const uint8_t *xa = (const uint8_t *)Xd + (size_t)r0 * row_bytes;
+        CU(stca::cc_gemm(h->bf16, xa, d, h->L[i].W1h, 2 * rd, h->proj_h.p, rd, nullptr, 0, rows, 2 * rd, d, 1.f,
+                         stca::EPI_SWIGLU, st));
+        CU(stca::cc_gemm(h->bf16, h->proj_h.p, rd, h->L[i].Woh, d, nullptr, 0, h->proj_y.as<float>(), d, rows, d, rd,
+                         1.f, stca::EPI_STORE, st));
+        uint8_t *dst = (uint8_t *)h->xt_cache.p + ((size_t)i * T2 + r0) * row_bytes;
+        CU(stca::cc_layernorm(h->bf16, h->proj_y.as<float>(), d, h->L[i].gh, h->L[i].bh, h->cfg.ln_eps, dst, d, rows,
+                              d, st));
+      }
+    }
+  }
+  h->B = B;
+  return STCA_OK;
+}
+
+// ===========================================================================
+// forward
+// ===========================================================================
+static stca_status ffn_rows(stca_handle *h, const void *in, int64_t ldi, int64_t rows, void *W1, void *Wo,
+                            const stca::TcWeights *tcw, int which, const float *g, const float *b, void *out_s,
+                            int64_t ldo, float *out_f, int64_t ldof, cudaStream_t st) {
+  // SwiGLUFFN (+ LN when g != null) on `rows` rows: the query-side instances of Eq.(1), (3), (7), (9)
+  const int d = h->cfg.d, rd = h->cfg.r * d, es = h->es;
+  if (rows <= 0) return STCA_OK;
+  if (h->bf16 && stca::tc_available()) {
+    CU(stca::tc_ffn(in, ldi, rows, which == 0 ? tcw->W1h : tcw->W1q, which == 0 ? tcw->Woh : tcw->Woq, d, rd, g, b,
+                    h->cfg.ln_eps, out_s, ldo, out_f, ldof, st));
+    return STCA_OK;
+  }
+  CU(h->hbuf.ensure((size_t)rows * rd * es));
+  CU(h->ybuf32.ensure((size_t)rows * d * 4));
+  CU(stca::cc_gemm(h->bf16, in, ldi, W1, 2 * rd, h->hbuf.p, rd, nullptr, 0, (int)rows, 2 * rd, d, 1.f,
+                   stca::EPI_SWIGLU, st));
+  if (g) {
+    CU(stca::cc_gemm(h->bf16, h->hbuf.p, rd, Wo, d, nullptr, 0, h->ybuf32.as<float>(), d, (int)rows, d, rd, 1.f,
+                     stca::EPI_STORE, st));
+    CU(stca::cc_layernorm(h->bf16, h->ybuf32.as<float>(), d, g, b, h->cfg.ln_eps, out_s, ldo, rows, d, st));
+  } else {
+    CU(stca::cc_gemm(h->bf16, h->hbuf.p, rd, Wo, d, out_s, ldo, out_f, ldof, (int)rows, d, rd, 1.f, stca::EPI_STORE,
+                     st));
+  }
+  return STCA_OK;
+}
+
+static stca_status gemm(stca_handle *h, const void *A, int64_t lda, const void *Bw, const void *Btc, int64_t ldb,
+                        void *Cs, int64_t ldcs, float *Cf, int64_t ldcf, int64_t M, int N, int K, cudaStream_t st) {
+  if (M <= 0) return STCA_OK;
+  if (h->bf16 && stca::tc_available()) {
+    CU(stca::tc_gemm(A, lda, Btc, M, N, K, Cs, ldcs, Cf, ldcf, st));
+    return STCA_OK;
+  }
+  CU(stca::cc_gemm(h->bf16, A, lda, Bw, ldb, Cs, ldcs, Cf, ldcf, (int)M, N, K, 1.f, stca::EPI_STORE, st));
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                                    float *out_Z, float *out_z, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (h->B < 0) return fail(h, STCA_ERR_STATE, "stca_forward before stca_project_history");
+  if (B != h->B) return fail(h, STCA_ERR_STATE, "B=%lld differs from the projected B=%lld", (long long)B, (long long)h->B);
+  if (Nt < 0 || !tgt_off || (Nt > 0 && (!xt || !out_Z)))
+    return fail(h, STCA_ERR_INVALID_ARG, "NULL or negative argument");
+  if (out_z && !h->cfg.with_z) return fail(h, STCA_ERR_INVALID_ARG, "out_z given but the handle has with_z = 0");
+  int64_t badi = -1;
+  stca_status s = check_offsets(tgt_off, B, Nt, false, &badi);
+  if (s != STCA_OK) return fail(h, s, "tgt_off invalid at request %lld (off[B]=%lld, Nt=%lld)", (long long)badi,
+                                (long long)tgt_off[B], (long long)Nt);
+  if (Nt == 0) return STCA_OK;
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = h->cfg.d, hh = h->cfg.h, M = h->cfg.M, es = h->es;
+  const int64_t NQ = Nt * hh;  // query rows (target, head)
+  const int64_t ldo = (int64_t)(M + 1) * d;
+
+  // inputs: x_t into block 0 of the concatenation buffer [x_t | o1 | ... | oM] (R10)
+  const void *xtd = xt;
+  if (!is_device_ptr(xt)) {
+    CU(h->xtin.ensure((size_t)Nt * d * es));
+    CU(cudaMemcpyAsync(h->xtin.p, xt, (size_t)Nt * d * es, cudaMemcpyHostToDevice, st));
+    xtd = h->xtin.p;
+  }
+  float *Zd = out_Z, *zd = out_z;
+  const bool Z_host = !is_device_ptr(out_Z), z_host = out_z && !is_device_ptr(out_z);
+  if (Z_host) {
+    CU(h->Zout.ensure((size_t)Nt * M * d * 4));
+    Zd = h->Zout.as<float>();
+  }
+  if (z_host) {
+    CU(h->zout.ensure((size_t)Nt * d * 4));
+    zd = h->zout.as<float>();
+  }
+  CU(h->ocat.ensure((size_t)Nt * ldo * es));
+  CU(h->q.ensure((size_t)Nt * d * es));
+  CU(h->c.ensure((size_t)Nt * d * es));
+  CU(h->U.ensure((size_t)NQ * d * es));
+  CU(h->Y.ensure((size_t)NQ * d * es));
+  CU(stca::copy_rows_strided(xtd, (int64_t)d * es, h->ocat.p, ldo * es, Nt, d * es, st));
+
+  // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
+  const bool tc_attn = h->bf16 && stca::tc_available() && stca::tc_attention_supported(d);
+  const int qtile = tc_attn ? 128 : 16;
+  std::vector<int64_t> it6;
+  int64_t nit = stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, nullptr, 0);
+  it6.resize((size_t)std::max<int64_t>(nit, 1) * 6);
+  stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, it6.data(), nit);
+  std::vector<int64_t> part_base(B, -1);
+  std::vector<stca::MergeItem> mi;
+  int64_t part_rows = 0;
+  int max_rows = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
+    const int32_t nc = stca_plan_chunks(h->len[b], (int32_t)h->chunk_cap, nullptr);
+    if (rows == 0 || nc <= 1) continue;
+    part_base[b] = part_rows;
+    mi.push_back({tgt_off[b] * hh, part_rows, (int32_t)rows, nc});
+    part_rows += rows * nc;
+    max_rows = std::max<int>(max_rows, (int)rows);
+  }
+  std::vector<stca::AttnItem> items((size_t)nit);
+  for (int64_t i = 0; i < nit; ++i) {
+    const int64_t *o = &it6[6 * i];
+    const int64_t b = o[0];
+    stca::AttnItem &a = items[i];
+    a.qrow0 = o[1];
+    a.nq = (int32_t)o[2];
+    a.key0 = h->coff[b] + o[3];
+    a.klen = (int32_t)o[4];
+    a.chunk = (int32_t)o[5];
+    a.pad = 0;
+    a.part_row = part_base[b] < 0 ? -1 : part_base[b] + o[5] * (tgt_off[b + 1] - tgt_off[b]) * hh + (o[1] - tgt_off[b] * hh);
+  }
+  const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
+  CU(h->items.ensure(items_bytes + 64));
+  CU(h->mitems.ensure(mi_bytes + 64));
+  CU(h->pin.ensure(items_bytes + mi_bytes + 64));
+  CU(cudaStreamSynchronize(st));  // the pinned staging buffer may still feed an earlier copy
+  memcpy(h->pin.p, items.data(), items_bytes);
+  memcpy((uint8_t *)h->pin.p + items_bytes, mi.data(), mi_bytes);
+  if (items_bytes) CU(cudaMemcpyAsync(h->items.p, h->pin.p, items_bytes, cudaMemcpyHostToDevice, st));
+  if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, (uint8_t *)h->pin.p + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
+  if (part_rows) CU(h->part.ensure((size_t)part_rows * (d + 2) * 4));
+
+  // a2: q(1) = LN(SwiGLUFFN(1)(x_t)), Eq.(3)
+  LayerW &L1 = h->L[0];
+  s = ffn_rows(h, h->ocat.p, ldo, Nt, L1.W1q, L1.Woq, &L1.tc, 1, L1.gq, L1.bq, h->q.p, d, nullptr, 0, st);
+  if (s != STCA_OK) return s;
+  for (int i = 1; i <= M; ++i) {
+    LayerW &Ly = h->L[i - 1];
+    const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)(i - 1) * h->T2 * d * es;
+    // a3: U = q W_QK (all heads; pre-scaled by log2(e)/sqrt(d_h)) -> [Nt h x d]
+    s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
+    if (s != STCA_OK) return s;
+    // a4: ragged single-query attention per request, reordered form Eq.(13)
+    if (tc_attn) {
+      CU(stca::tc_attention(h->U.p, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+    } else {
+      CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+    }
+    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows,
+                            h->part.as<float>(), d, h->Y.p, st));
+    // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
+    s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,
+             Zd + (size_t)(i - 1) * d, (int64_t)M * d, Nt, d, hh * d, st);
+    if (s != STCA_OK) return s;
+    // a6: q(i+1) = SwiGLUFFN(i+1)([o(1)..o(i) | x_t] W_C(i+1)), Eq.(7)
+    if (i < M) {
+      LayerW &Ln = h->L[i];
+      s = gemm(h, h->ocat.p, ldo, Ln.WC, Ln.tc.WC, d, h->c.p, d, nullptr, 0, Nt, d, (i + 1) * d, st);
+      if (s != STCA_OK) return s;
+      s = ffn_rows(h, h->c.p, d, Nt, Ln.W1q, Ln.Woq, &Ln.tc, 1, nullptr, nullptr, h->q.p, d, nullptr, 0, st);
+      if (s != STCA_OK) return s;
+    }
+  }
+  // a7: z = SwiGLUFFN_Z([o(1)..o(M) | x_t] W_Z), Eq.(9)
+  if (zd) {
+    s = gemm(h, h->ocat.p, ldo, h->WZ, h->tcz.WC, d, h->c.p, d, nullptr, 0, Nt, d, (M + 1) * d, st);
+    if (s != STCA_OK) return s;
+    s = ffn_rows(h, h->c.p, d, Nt, h->W1z, h->Woz, &h->tcz, 0, nullptr, nullptr, nullptr, 0, zd, d, st);
+    if (s != STCA_OK) return s;
+  }
+  if (Z_host) CU(cudaMemcpyAsync(out_Z, Zd, (size_t)Nt * M * d * 4, cudaMemcpyDeviceToHost, st));
+  if (z_host) CU(cudaMemcpyAsync(out_z, zd, (size_t)Nt * d * 4, cudaMemcpyDeviceToHost, st));
+  if (Z_host || z_host) CU(cudaStreamSynchronize(st));
+  CU(cudaGetLastError());
+  return STCA_OK;
+}

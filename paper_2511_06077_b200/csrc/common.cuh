@@ -1,0 +1,48 @@
+// common.cuh -- shared device helpers of libstca (product path only; never used by oracle/).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace stca {
+
+typedef __nv_bfloat16 bf16;
+
+// storage-type conversions (fp32 accumulation everywhere)
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(bf16 x) { return __bfloat162float(x); }
+template <typename S> __device__ __forceinline__ S from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Device-side attention work item (host plan -> device), 48 bytes.
+struct AttnItem {
+  int64_t qrow0;     // first query row (row index into U / Y, = target*h + head)
+  int64_t key0;      // first key row in the compacted X~ cache
+  int64_t part_row;  // -1: single-chunk request (write normalised Y); else partial row of q=0
+  int32_t nq;        // query rows in this item
+  int32_t klen;      // keys in this item
+  int32_t chunk;     // chunk index within the request
+  int32_t pad;
+};
+
+// Merge item: one multi-chunk request.
+struct MergeItem {
+  int64_t qrow0;     // first query row of the request
+  int64_t part_row;  // partial row of (chunk 0, q = 0)
+  int32_t rows;      // m_b * h
+  int32_t nchunks;
+};
+
+}  // namespace stca

@@ -1,0 +1,355 @@
+// kernels_cc.cu -- CUDA-core kernels: the fp32 path (STCA_FP32, 1e-4 parity) and
+// utility kernels shared by both paths.  SURVEY §2.2 K-G; Eq.(1)-(9).
+#include <math.h>
+
+#include "launch.h"
+
+namespace stca {
+
+// --------------------------------------------------------------------------
+// tiled SGEMM-style GEMM, 64x64 tile, BK 16, 256 threads, 4x4 per thread
+// --------------------------------------------------------------------------
+template <typename S, int EPI>
+__global__ void __launch_bounds__(256) k_cc_gemm(const S *__restrict__ A, int64_t lda, const S *__restrict__ B,
+                                                 int64_t ldb, S *__restrict__ Cs, int64_t ldcs,
+                                                 float *__restrict__ Cf, int64_t ldcf, int M, int N, int K,
+                                                 float alpha) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      int r = i / 16, c = i % 16;  // A tile: 64 rows x 16 k
+      int64_t gm = m0 + r;
+      int gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? to_f(A[gm * lda + gk]) : 0.f;
+      int rb = i / 64, cb = i % 64;  // B tile: 16 k x 64 cols
+      int gkb = k0 + rb;
+      int64_t gn = n0 + cb;
+      Bs[rb][cb] = (gkb < K && gn < N) ? to_f(B[(int64_t)gkb * ldb + gn]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+    if (EPI == EPI_STORE) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t gn = n0 + tx * 4 + j;
+        if (gn >= N) continue;
+        float v = alpha * acc[i][j];
+        if (Cs) Cs[gm * ldcs + gn] = from_f<S>(v);
+        if (Cf) Cf[gm * ldcf + gn] = v;
+      }
+    } else {  // SWIGLU: cols (2j, 2j+1) = (u_j, v_j) -> u * v * sigmoid(v), Eq.(1)
+#pragma unroll
+      for (int j = 0; j < 4; j += 2) {
+        int64_t gn = n0 + tx * 4 + j;
+        if (gn >= N) continue;
+        float u = acc[i][j], v = acc[i][j + 1];
+        float hv = u * (v / (1.f + expf(-v)));
+        Cs[gm * ldcs + gn / 2] = from_f<S>(hv);
+      }
+    }
+  }
+}
+
+cudaError_t cc_gemm(bool is_bf16, const void *A, int64_t lda, const void *B, int64_t ldb, void *Cs, int64_t ldcs,
+                    float *Cf, int64_t ldcf, int M, int N, int K, float alpha, int epi, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  note_launch();
+#define LAUNCH(S, E)                                                                                        \
+  k_cc_gemm<S, E><<<grid, 256, 0, st>>>((const S *)A, lda, (const S *)B, ldb, (S *)Cs, ldcs, Cf, ldcf, M, N, \
+                                        K, alpha)
+  if (is_bf16) {
+    if (epi == EPI_STORE) LAUNCH(bf16, EPI_STORE); else LAUNCH(bf16, EPI_SWIGLU);
+  } else {
+    if (epi == EPI_STORE) LAUNCH(float, EPI_STORE); else LAUNCH(float, EPI_SWIGLU);
+  }
+#undef LAUNCH
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------
+// LayerNorm over rows, warp per row (biased variance, eps inside the sqrt)
+// --------------------------------------------------------------------------
+template <typename S>
+__global__ void k_layernorm(const float *__restrict__ in, int64_t ldi, const float *__restrict__ g,
+                            const float *__restrict__ b, float eps, S *__restrict__ out, int64_t ldo, int64_t rows,
+                            int d) {
+  int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float *x = in + row * ldi;
+  float s = 0.f;
+  for (int e = lane; e < d; e += 32) s += x[e];
+  float mu = warp_sum(s) / d;
+  float v = 0.f;
+  for (int e = lane; e < d; e += 32) {
+    float t = x[e] - mu;
+    v += t * t;
+  }
+  float inv = rsqrtf(warp_sum(v) / d + eps);
+  for (int e = lane; e < d; e += 32) out[row * ldo + e] = from_f<S>((x[e] - mu) * inv * g[e] + b[e]);
+}
+
+cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float *g, const float *b, float eps,
+                         void *out, int64_t ldo, int64_t rows, int d, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  int64_t blocks = (rows + 7) / 8;
+  note_launch();
+  if (is_bf16)
+    k_layernorm<bf16><<<(unsigned)blocks, 256, 0, st>>>(in, ldi, g, b, eps, (bf16 *)out, ldo, rows, d);
+  else
+    k_layernorm<float><<<(unsigned)blocks, 256, 0, st>>>(in, ldi, g, b, eps, (float *)out, ldo, rows, d);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------
+// CUDA-core ragged single-query attention (reordered form, Eq.(13)).
+// One CTA per work item: <= 16 query rows (2 per warp), keys streamed in tiles of 32
+// through shared memory, online softmax in the log2 domain (U is pre-scaled by
+// log2(e)/sqrt(d_h)).  Writes normalised Y rows (single-chunk requests) or
+// (m, l, O) partials.
+// --------------------------------------------------------------------------
+template <typename S>
+__global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, const S *__restrict__ Xt,
+                                                      const AttnItem *__restrict__ items, int d,
+                                                      S *__restrict__ Y, float *__restrict__ part) {
+  extern __shared__ float sm[];
+  const AttnItem it = items[blockIdx.x];
+  const int dp = d + 1;  // padded row (bank conflicts)
+  float *Us = sm;             // [16][dp]
+  float *Xs = Us + 16 * dp;   // [32][dp]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < 16 * d; i += 256) {
+    int q = i / d, e = i % d;
+    Us[q * dp + e] = q < it.nq ? to_f(U[(it.qrow0 + q) * d + e]) : 0.f;
+  }
+  const int nd = (d + 31) / 32;  // dims per lane (<= 16)
+  float O[2][16];
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) O[rr][k] = 0.f;
+  for (int j0 = 0; j0 < it.klen; j0 += 32) {
+    __syncthreads();
+    const int nk = min(32, it.klen - j0);
+    for (int i = threadIdx.x; i < 32 * d; i += 256) {
+      int j = i / d, e = i % d;
+      Xs[j * dp + e] = j < nk ? to_f(Xt[(it.key0 + j0 + j) * d + e]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int q = warp * 2 + rr;
+      if (q >= it.nq) continue;  // warp-uniform
+      float s = 0.f;
+      const float *ur = Us + q * dp, *xr = Xs + lane * dp;
+      for (int e = 0; e < d; ++e) s = fmaf(ur[e], xr[e], s);
+      if (lane >= nk) s = -INFINITY;
+      float tmax = warp_max(s);
+      float mnew = fmaxf(mrow[rr], tmax);
+      float corr = exp2f(mrow[rr] - mnew);  // exp2(-inf) = 0 on the first tile
+      float p = exp2f(s - mnew);
+      lrow[rr] = lrow[rr] * corr + warp_sum(p);
+      mrow[rr] = mnew;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) O[rr][k] *= corr;
+      for (int j = 0; j < nk; ++j) {
+        float pj = __shfl_sync(0xffffffffu, p, j);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          int e = lane + 32 * k;
+          if (k < nd && e < d) O[rr][k] = fmaf(pj, Xs[j * dp + e], O[rr][k]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int q = warp * 2 + rr;
+    if (q >= it.nq) continue;
+    if (it.part_row < 0) {
+      const float inv = 1.f / lrow[rr];
+      for (int k = 0; k < nd; ++k) {
+        int e = lane + 32 * k;
+        if (e < d) Y[(it.qrow0 + q) * d + e] = from_f<S>(O[rr][k] * inv);
+      }
+    } else {
+      float *pr = part + (it.part_row + q) * (int64_t)(d + 2);
+      if (lane == 0) {
+        pr[0] = mrow[rr];
+        pr[1] = lrow[rr];
+      }
+      for (int k = 0; k < nd; ++k) {
+        int e = lane + 32 * k;
+        if (e < d) pr[2 + e] = O[rr][k];
+      }
+    }
+  }
+}
+
+cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const AttnItem *items, int64_t n_items, int d,
+                         void *Y, float *part, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  size_t smem = sizeof(float) * (16 + 32) * (d + 1);
+  note_launch();
+  if (is_bf16) {
+    cudaFuncSetAttribute(k_cc_attention<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cc_attention<bf16><<<(unsigned)n_items, 256, smem, st>>>((const bf16 *)U, (const bf16 *)Xt, items, d,
+                                                               (bf16 *)Y, part);
+  } else {
+    cudaFuncSetAttribute(k_cc_attention<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cc_attention<float><<<(unsigned)n_items, 256, smem, st>>>((const float *)U, (const float *)Xt, items, d,
+                                                                (float *)Y, part);
+  }
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------
+// split-K LSE merge (K-E): fold chunks 0..C-1 in order, per query row
+//   mu* = max_c mu_c; l* = sum_c 2^(mu_c - mu*) l_c; Y = sum_c 2^(mu_c - mu*) O_c / l*
+// grid: (items, row blocks of 8 rows), warp per row.
+// --------------------------------------------------------------------------
+template <typename S>
+__global__ void k_merge(const MergeItem *__restrict__ items, const float *__restrict__ part, int d,
+                        S *__restrict__ Y) {
+  const MergeItem it = items[blockIdx.x];
+  const int q = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (q >= it.rows) return;
+  const int64_t stride = (int64_t)it.rows * (d + 2);
+  const float *p0 = part + (it.part_row + q) * (int64_t)(d + 2);
+  float mu = -INFINITY;
+  for (int c = 0; c < it.nchunks; ++c) mu = fmaxf(mu, p0[c * stride]);
+  float l = 0.f;
+  for (int c = 0; c < it.nchunks; ++c) l += exp2f(p0[c * stride] - mu) * p0[c * stride + 1];
+  const float inv = 1.f / l;
+  for (int e = lane; e < d; e += 32) {
+    float acc = 0.f;
+    for (int c = 0; c < it.nchunks; ++c) acc += exp2f(p0[c * stride] - mu) * p0[c * stride + 2 + e];
+    Y[(it.qrow0 + q) * d + e] = from_f<S>(acc * inv);
+  }
+}
+
+cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
+                           int d, void *Y, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  dim3 grid((unsigned)n_items, (unsigned)((max_rows + 7) / 8));
+  note_launch();
+  if (is_bf16)
+    k_merge<bf16><<<grid, 256, 0, st>>>(items, part, d, (bf16 *)Y);
+  else
+    k_merge<float><<<grid, 256, 0, st>>>(items, part, d, (float *)Y);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------
+// utilities
+// --------------------------------------------------------------------------
+__global__ void k_gather_rows(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst,
+                              const int64_t *__restrict__ seg, int row_bytes) {
+  const int64_t s = seg[blockIdx.y * 3 + 0], t = seg[blockIdx.y * 3 + 1], n = seg[blockIdx.y * 3 + 2];
+  const int64_t bytes = n * row_bytes;
+  const int64_t words = bytes / 16;  // row_bytes is a multiple of 16
+  const int4 *s4 = reinterpret_cast<const int4 *>(src + s * row_bytes);
+  int4 *t4 = reinterpret_cast<int4 *>(dst + t * row_bytes);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    t4[i] = s4[i];
+}
+
+cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg, int64_t nseg, int64_t max_len,
+                        int row_bytes, cudaStream_t st) {
+  if (nseg <= 0) return cudaSuccess;
+  int64_t words = max_len * row_bytes / 16;
+  unsigned gx = (unsigned)((words + 255) / 256);
+  if (gx > 64) gx = 64;
+  if (gx < 1) gx = 1;
+  note_launch();
+  k_gather_rows<<<dim3(gx, (unsigned)nseg), 256, 0, st>>>((const uint8_t *)src, (uint8_t *)dst, seg, row_bytes);
+  return cudaGetLastError();
+}
+
+__global__ void k_copy_rows(const uint8_t *__restrict__ src, int64_t lds, uint8_t *__restrict__ dst, int64_t ldd,
+                            int64_t rows, int row_bytes) {
+  const int w = row_bytes / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * w; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / w, c = i % w;
+    reinterpret_cast<uint32_t *>(dst + r * ldd)[c] = reinterpret_cast<const uint32_t *>(src + r * lds)[c];
+  }
+}
+
+cudaError_t copy_rows_strided(const void *src, int64_t lds, void *dst, int64_t ldd, int64_t rows, int row_bytes,
+                              cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  int64_t n = rows * (row_bytes / 4);
+  unsigned g = (unsigned)((n + 255) / 256);
+  if (g > 4096) g = 4096;
+  note_launch();
+  k_copy_rows<<<g, 256, 0, st>>>((const uint8_t *)src, lds, (uint8_t *)dst, ldd, rows, row_bytes);
+  return cudaGetLastError();
+}
+
+__global__ void k_f32_to_bf16(const float *__restrict__ s, bf16 *__restrict__ t, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    t[i] = __float2bfloat16_rn(s[i]);
+}
+
+cudaError_t f32_to_bf16(const float *src, bf16 *dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  unsigned g = (unsigned)((n + 255) / 256);
+  if (g > 8192) g = 8192;
+  note_launch();
+  k_f32_to_bf16<<<g, 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+// W_QK^r = W_Q^r W_K^r^T (scaled) and W_VO^r = W_V^r W_O^r, one thread per output element.
+__global__ void k_prep_qk_vo(const float *__restrict__ WQ, const float *__restrict__ WK,
+                             const float *__restrict__ WV, const float *__restrict__ WO, int d, int h, float scale,
+                             float *__restrict__ WQK, float *__restrict__ WVO) {
+  const int dh = d / h;
+  const int64_t total = (int64_t)h * d * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(i / ((int64_t)d * d));
+    int e = (int)((i / d) % d), f = (int)(i % d);
+    float qk = 0.f, vo = 0.f;
+    for (int c = 0; c < dh; ++c) {
+      qk = fmaf(WQ[(int64_t)e * d + r * dh + c], WK[(int64_t)f * d + r * dh + c], qk);
+      vo = fmaf(WV[(int64_t)e * d + r * dh + c], WO[(int64_t)(r * dh + c) * d + f], vo);
+    }
+    WQK[(int64_t)e * (h * d) + (int64_t)r * d + f] = qk * scale;
+    WVO[((int64_t)r * d + e) * d + f] = vo;
+  }
+}
+
+cudaError_t prep_qk_vo(const float *WQ, const float *WK, const float *WV, const float *WO, int d, int h,
+                       float qk_scale, float *WQK, float *WVO, cudaStream_t st) {
+  int64_t total = (int64_t)h * d * d;
+  unsigned g = (unsigned)((total + 255) / 256);
+  if (g > 16384) g = 16384;
+  note_launch();
+  k_prep_qk_vo<<<g, 256, 0, st>>>(WQ, WK, WV, WO, d, h, qk_scale, WQK, WVO);
+  return cudaGetLastError();
+}
+
+}  // namespace stca

@@ -1,0 +1,40 @@
+// launch.h -- internal host-side launchers (C++ linkage, internal to libstca.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace stca {
+
+enum Epi { EPI_STORE = 0, EPI_SWIGLU = 1 };
+
+// process-wide count of kernels launched by libstca (stca_kernel_launches())
+void note_launch(int n = 1);
+
+// ---- CUDA-core kernels (fp32 path; reference-grade, K-G of SURVEY §2.2) ----
+// C = alpha * A[MxK] B[KxN]; A, B row-major storage S (lda, ldb);
+// EPI_STORE: Cs (S, ldcs) and/or Cf (fp32, ldcf) get alpha*acc (either may be null);
+// EPI_SWIGLU: B columns interleaved (u_j, v_j); Cs[:, j] = u_j * silu(v_j), N/2 output cols.
+cudaError_t cc_gemm(bool is_bf16, const void *A, int64_t lda, const void *B, int64_t ldb, void *Cs, int64_t ldcs,
+                    float *Cf, int64_t ldcf, int M, int N, int K, float alpha, int epi, cudaStream_t st);
+// out (S, ldo) = LN(in fp32 [rows x d], ld) * g + b
+cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float *g, const float *b, float eps,
+                         void *out, int64_t ldo, int64_t rows, int d, cudaStream_t st);
+// online-softmax sweep over items (qtile <= 16 rows per item)
+cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const AttnItem *items, int64_t n_items, int d,
+                         void *Y, float *part, cudaStream_t st);
+cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
+                           int d, void *Y, cudaStream_t st);
+
+// ---- utility kernels ----
+cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg /*[n][3]: src,dst,len*/, int64_t nseg,
+                        int64_t max_len, int row_bytes, cudaStream_t st);
+cudaError_t copy_rows_strided(const void *src, int64_t lds, void *dst, int64_t ldd, int64_t rows, int row_bytes,
+                              cudaStream_t st);
+cudaError_t f32_to_bf16(const float *src, bf16 *dst, int64_t n, cudaStream_t st);
+// WQK[e][r*d+f] = scale * sum_c WQ[e][r dh + c] WK[f][r dh + c];  WVO[r*d+e][f] = sum_c WV[e][r dh+c] WO[r dh+c][f]
+cudaError_t prep_qk_vo(const float *WQ, const float *WK, const float *WV, const float *WO, int d, int h,
+                       float qk_scale, float *WQK, float *WVO, cudaStream_t st);
+
+}  // namespace stca

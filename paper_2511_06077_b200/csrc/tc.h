@@ -1,0 +1,53 @@
+// tc.h -- tcgen05 / TMEM / TMA kernels of the bf16 path (sm_100a), internal interface.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+
+#include "common.cuh"
+
+namespace stca {
+
+// Repacked bf16 weights in K-major ("B^T", [N x K] row-major) layouts for TMA/UMMA.
+struct TcWeights {
+  void *W1h = nullptr;  // SwiGLU first GEMM, chunk-interleaved [u chunk | v chunk] rows, [2 rd x d]
+  void *Woh = nullptr;  // W_o^T [d x rd]
+  void *W1q = nullptr, *Woq = nullptr;  // query FFN of this layer (aliases W1h/Woh under reading R5)
+  void *WQK = nullptr;  // W_QK^T [h d x d]
+  void *WVO = nullptr;  // W_VO^T [d x h d]
+  void *WC = nullptr;   // permuted W_C^T [d x i d] (or W_Z^T)
+};
+
+typedef std::function<void *(size_t)> DevAlloc;
+
+struct TcProj {
+  const void *X = nullptr;  // [rows x d] bf16
+  int64_t rows = 0;
+  int d = 0, rd = 0, M = 0;
+  float eps = 1e-5f;
+  const void *W1[16] = {}, *Wo[16] = {};
+  const float *g[16] = {}, *b[16] = {};
+  void *out = nullptr;            // layer i at out + i * out_layer_stride elements (bf16)
+  int64_t out_layer_stride = 0;
+};
+
+bool tc_available();                       // sm_100a tensor-core path compiled in and usable
+bool tc_attention_supported(int d);
+bool tc_prepare_ffn(const float *Wu, const float *Wv, const float *Wo, int d, int rd, TcWeights *tc,
+                    const DevAlloc &alloc);
+// WQK/WVO: device bf16 row-major [d x hd] / [hd x d]; WC: device bf16 row-major [(i) d x d] (may be null)
+bool tc_prepare_layer(const void *WQK, const void *WVO, const void *WC, int i, int d, int h, TcWeights *tc,
+                      const DevAlloc &alloc);
+cudaError_t tc_project(const TcProj &p, cudaStream_t st);
+// SwiGLUFFN (+LN if g) over rows; outputs bf16 (out_s, ldo) and/or fp32 (out_f, ldof)
+cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, const void *Wo, int d, int rd,
+                   const float *g, const float *b, float eps, void *out_s, int64_t ldo, float *out_f, int64_t ldof,
+                   cudaStream_t st);
+// C[M x N] = A[M x K] (bf16, lda) . B where Bt = B^T [N x K] bf16 K-major
+cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
+                    float *Cf, int64_t ldcf, cudaStream_t st);
+cudaError_t tc_attention(const void *U, const void *Xt, int64_t T2, const AttnItem *items, int64_t n_items, int d,
+                         void *Y, float *part, cudaStream_t st);
+
+}  // namespace stca

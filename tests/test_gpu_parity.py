@@ -1,0 +1,149 @@
+"""GPU parity: the CUDA path (through the C ABI) against the f64 oracle on the same
+seeded inputs.  Tolerances (north star, R20): row-infinity-relative error
+per (target, layer) <= 1e-4 on the fp32 path and <= 2e-2 on the bf16 path; all
+offset / indexing work exact (checked through bit-exact invariances)."""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from _util import make_cfg, rowrel, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+def check(wl, Z, z, tol, nthreads=8, **kw):
+    Zr, zr, rows = oracle.forward_workload(wl, nthreads=nthreads, **kw)
+    eZ = rowrel(Z[rows], Zr)
+    assert np.isfinite(Z[rows]).all()
+    assert eZ.max() <= tol, (eZ.max(), np.unravel_index(eZ.argmax(), eZ.shape))
+    if z is not None:
+        ez = rowrel(z[rows], zr)
+        assert ez.max() <= tol, ez.max()
+    return eZ.max()
+
+
+def test_tiny_fp32():
+    wl = workload.make_workload("tiny", seed=0)
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["fp32"])
+
+
+RAGGED = dict(lengths=np.array([1, 64, 200, 4097, 5000, 130, 9000]), m=[3, 0, 16, 64, 2, 33, 5])
+
+
+def ragged_workload(dtype, d=128, h=4, M=4, L_infer=4500, seed=1, ln_affine=True, wq_scale=1.0):
+    lengths = RAGGED["lengths"]
+    cfg = make_cfg(B=len(lengths), d=d, h=h, M=M, dtype=dtype, L_infer=L_infer)
+    wl = workload.make_workload(cfg, seed=seed, lengths=lengths, ln_affine=ln_affine, wq_scale=wq_scale)
+    # ragged target counts (m_b = 0 allowed)
+    m = np.array(RAGGED["m"], dtype=np.int64)
+    wl.tgt_off = np.concatenate([[0], np.cumsum(m)]).astype(np.int64)
+    wl.xt = wl.xt[: wl.tgt_off[-1]] if wl.xt.shape[0] >= wl.tgt_off[-1] else np.resize(wl.xt, (wl.tgt_off[-1], d))
+    rng = np.random.default_rng(seed + 100)
+    xt = rng.standard_normal((int(wl.tgt_off[-1]), d), dtype=np.float32)
+    if dtype == "bf16":
+        wl.xt_bits = workload.bf16_bits(xt).reshape(xt.shape)
+        wl.xt = workload.bits_to_f32(wl.xt_bits).reshape(xt.shape)
+    else:
+        wl.xt = xt
+    return wl
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_ragged_multichunk_suffix(dtype):
+    wl = ragged_workload(dtype)
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL[dtype])
+
+
+@pytest.mark.parametrize("d,h", [(64, 2), (256, 8)])
+def test_bf16_other_widths(d, h):
+    wl = ragged_workload("bf16", d=d, h=h, M=3, L_infer=0)
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["bf16"])
+
+
+def test_bf16_sharp_softmax():
+    """W_Q x 8 ("sharp" regime of SURVEY §8(c)): still inside the 2e-2 bound."""
+    wl = ragged_workload("bf16", wq_scale=8.0)
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["bf16"])
+
+
+def test_rlb_and_batch_invariance_bit_exact():
+    """P10/P18: a request's outputs are bit-identical alone or inside any batch."""
+    wl = ragged_workload("bf16")
+    Z, z = run_gpu(wl)
+    for b in (2, 3, 6):
+        sub = workload.Workload(cfg=wl.cfg, seed=0, weights=wl.weights, lengths=wl.lengths[b:b + 1],
+                                hist_off=np.array([0, wl.lengths[b]]),
+                                tgt_off=np.array([0, wl.tgt_off[b + 1] - wl.tgt_off[b]]),
+                                X=wl.X[wl.hist_off[b]:wl.hist_off[b + 1]], xt=wl.xt[wl.tgt_off[b]:wl.tgt_off[b + 1]],
+                                X_bits=wl.X_bits[wl.hist_off[b]:wl.hist_off[b + 1]],
+                                xt_bits=wl.xt_bits[wl.tgt_off[b]:wl.tgt_off[b + 1]])
+        Zb, zb = run_gpu(sub)
+        t0, t1 = wl.tgt_off[b], wl.tgt_off[b + 1]
+        assert np.array_equal(Zb, Z[t0:t1]) and np.array_equal(zb, z[t0:t1]), b
+
+
+def test_host_buffers_equal_device_buffers():
+    wl = ragged_workload("bf16")
+    Zd, zd = run_gpu(wl)
+    Zh, zh = run_gpu(wl, host=True)
+    assert np.array_equal(Zd, Zh) and np.array_equal(zd, zh)
+
+
+def test_single_key_history_exact_weight():
+    """P4: L_b = 1 -> alpha = 1: the attention output is the (bf16) X~ row itself, so o is
+    independent of the query; two different targets give identical Z."""
+    cfg = make_cfg(B=1, m=2, dtype="bf16", M=1)
+    wl = workload.make_workload(cfg, seed=4, lengths=np.array([1]))
+    Z, z = run_gpu(wl)
+    assert np.array_equal(Z[0, 0], Z[1, 0])
+    check(wl, Z, z, TOL["bf16"])
+
+
+def test_errors_leave_outputs_untouched():
+    import torch
+    import paper_2511_06077_b200 as stca
+    wl = ragged_workload("bf16")
+    c = wl.cfg
+    m = stca.STCA(workload.full_weights(wl), d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer)
+    X = torch.from_numpy(wl.X_bits.view(np.int16)).cuda()
+    bad = wl.hist_off.copy()
+    bad[2] = bad[1]  # request 1 empty
+    with pytest.raises(stca.StcaError) as e:
+        m.project_history(X, bad)
+    assert e.value.status == -4 and "1" in e.value.message
+    with pytest.raises(stca.StcaError) as e:
+        m.forward(torch.zeros(3, c.d, dtype=torch.int16, device="cuda"), [0, 3],
+                  torch.zeros(3, c.M, c.d, device="cuda"))
+    assert e.value.status == -6  # forward before project
+    m.project_history(X, wl.hist_off)
+    Z = torch.full((wl.Nt, c.M, c.d), float("nan"), device="cuda")
+    xt = torch.from_numpy(wl.xt_bits.view(np.int16)).cuda()
+    t = wl.tgt_off.copy()
+    t[-1] += 1
+    with pytest.raises(stca.StcaError) as e:
+        m.forward(xt, t, Z)
+    assert e.value.status == -3
+    torch.cuda.synchronize()
+    assert torch.isnan(Z).all()
+    with pytest.raises(stca.StcaError) as e:
+        stca.STCA({}, d=c.d, h=c.h, r=c.r, M=c.M)
+    assert e.value.status == -2 and "missing weight" in e.value.message
+
+
+@pytest.mark.parametrize("name", ["serve", "train"])
+def test_full_size_sampled(name):
+    """BASELINE configs at full size, in the bench's launch configuration; the oracle
+    checks a deterministic sample of requests (shortest, longest, first)."""
+    wl = workload.make_workload(name, seed=0)
+    Z, z = run_gpu(wl)
+    L = wl.lengths
+    sample = sorted({0, int(np.argmin(L)), int(np.argmax(L))})
+    check(wl, Z, z, TOL["bf16"], requests=sample)
+    assert np.isfinite(Z).all() and np.isfinite(z).all()
