@@ -1,0 +1,360 @@
+// tc_gemm.cu -- warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+//   C[M x N] = A[M x K] . Bt^T,   A bf16 row-major (lda), Bt = B^T bf16 [N x K] (K-major)
+//
+// Warp 0: TMA producer (SWIZZLE_128B boxes of 64 K-elements), warp 1: TMEM allocator +
+// single-thread tcgen05.mma issuer (M = 128, N-slices <= 256, K = 16 per instruction),
+// warps 2-5: epilogue, one thread per accumulator row (TMEM lane), reading the fp32
+// accumulator with tcgen05.ld.  Epilogues:
+//   TEPI_STORE  : alpha*acc -> bf16 (Cs) and/or fp32 (Cf)
+//   TEPI_SWIGLU : Bt rows chunk-interleaved [u_32c..u_32c+31 | v_32c..v_32c+31]:
+//                H[:, 32c+j] = u * silu(v) -> bf16   (Eq.(1))
+//   TEPI_LN     : BN == N == d: LayerNorm over the row (biased variance, eps inside sqrt)
+//                -> bf16 / fp32                       (Eq.(2)-(3))
+// Used for the target-side contractions (U = q W_QK, o = Y W_VO, [o|x_t] W_C, W_Z) and
+// the query-side SwiGLUFFN instances.
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "launch.h"
+#include "tc.h"
+#include "tc_ptx.cuh"
+
+namespace stca {
+namespace tc {
+
+enum { TEPI_STORE = 0, TEPI_SWIGLU = 1, TEPI_LN = 2 };
+
+struct EpiArgs {
+  bf16 *Cs;
+  int64_t ldcs;
+  float *Cf;
+  int64_t ldcf;
+  const float *g, *b;
+  float eps;
+};
+
+__device__ __forceinline__ float silu_f(float v) {  // v * sigmoid(v)
+  return __fdividef(v, 1.f + exp2f(-1.4426950408889634f * v));
+}
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int NS = BN < 256 ? BN : 256;  // N per MMA instruction
+  static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
+              int K, float alpha, EpiArgs ea) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE);
+  uint64_t *empty = full + C::STAGES;
+  uint64_t *tfull = empty + C::STAGES;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tfull + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
+  const int nk = (K + C::BK - 1) / C::BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::STAGES;
+        const uint32_t ph = (kb / C::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t *sa = smem + s * C::STAGE, *sb = sa + C::A_BYTES;
+        mbar_expect_tx(&full[s], C::STAGE);
+        tma_load_2d(sa, &mapA, &full[s], kb * C::BK, m0);
+#pragma unroll
+        for (int j = 0; j < BN / C::NS; ++j) tma_load_2d(sb + j * C::NS * 128, &mapB, &full[s], kb * C::BK, n0 + j * C::NS);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(128, C::NS, 0);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::STAGES;
+        const uint32_t ph = (kb / C::STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * C::STAGE), sb = sa + C::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k) {
+          const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
+#pragma unroll
+          for (int j = 0; j < BN / C::NS; ++j) {
+            const uint64_t bd = sdesc_sw128(sb + j * C::NS * 128 + k * 32, 16, 1024);
+            umma_f16_ss(tmem + j * C::NS, ad, bd, idesc, (kb | k) != 0);
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tfull);
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int64_t grow = (int64_t)m0 + row;
+    const bool ok = grow < M;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    if (EPI == TEPI_STORE) {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_ld_wait();
+        if (ok) {
+          if (ea.Cf) {
+            float4 *dst = reinterpret_cast<float4 *>(ea.Cf + grow * ea.ldcf + n0 + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              dst[i] = make_float4(alpha * __uint_as_float(r[4 * i]), alpha * __uint_as_float(r[4 * i + 1]),
+                                   alpha * __uint_as_float(r[4 * i + 2]), alpha * __uint_as_float(r[4 * i + 3]));
+          }
+          if (ea.Cs) {
+            uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + n0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16(alpha * __uint_as_float(r[8 * i]), alpha * __uint_as_float(r[8 * i + 1])),
+                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 2]), alpha * __uint_as_float(r[8 * i + 3])),
+                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 4]), alpha * __uint_as_float(r[8 * i + 5])),
+                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 6]), alpha * __uint_as_float(r[8 * i + 7])));
+          }
+        }
+      }
+    } else if (EPI == TEPI_SWIGLU) {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 64) {
+        uint32_t u[32], v[32];
+        tmem_ld32(taddr + c, u);
+        tmem_ld32(taddr + c + 32, v);
+        tmem_ld_wait();
+        if (ok) {
+          uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + (n0 + c) / 2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int e = 8 * i + 2 * j;
+              w[j] = pack_bf16(__uint_as_float(u[e]) * silu_f(__uint_as_float(v[e])),
+                               __uint_as_float(u[e + 1]) * silu_f(__uint_as_float(v[e + 1])));
+            }
+            dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    } else {  // TEPI_LN over BN == d columns
+      float s = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s += __uint_as_float(r[i]);
+      }
+      const float mu = s / BN;
+      float v2 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float t = __uint_as_float(r[i]) - mu;
+          v2 += t * t;
+        }
+      }
+      const float inv = rsqrtf(v2 / BN + ea.eps);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_ld_wait();
+        if (ok) {
+          float y[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) y[i] = (__uint_as_float(r[i]) - mu) * inv * __ldg(ea.g + c + i) + __ldg(ea.b + c + i);
+          if (ea.Cs) {
+            uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
+                                  pack_bf16(y[8 * i + 4], y[8 * i + 5]), pack_bf16(y[8 * i + 6], y[8 * i + 7]));
+          }
+          if (ea.Cf) {
+            float4 *dst = reinterpret_cast<float4 *>(ea.Cf + grow * ea.ldcf + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+// bf16 row-major [rows x cols] with leading dimension ld (elements); box = box_rows x 64, SWIZZLE_128B
+bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, float alpha,
+                               const EpiArgs &ea, cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  CUtensorMap ma, mb;
+  if (!make_map_bf16(&ma, A, M, K, lda, 128) || !make_map_bf16(&mb, Bt, N, K, K, C::NS)) return cudaErrorInvalidValue;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid((unsigned)((M + 127) / 128), (unsigned)(N / BN));
+  note_launch();
+  k_tc_gemm<BN, EPI><<<grid, 192, C::SMEM, st>>>(ma, mb, (int)M, N, K, alpha, ea);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+
+// dispatch on N (N % BN == 0; BN = min(N, 256) for STORE/SWIGLU, BN = N for LN)
+static cudaError_t gemm_dispatch(int epi, const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K,
+                                 const tc::EpiArgs &ea, cudaStream_t st) {
+  using namespace tc;
+  if (M <= 0) return cudaSuccess;
+  if (K % 64 || N % 32) return cudaErrorInvalidValue;
+#define G(BN, E) return launch_gemm<BN, E>(A, lda, Bt, M, N, K, 1.f, ea, st)
+  if (epi == TEPI_LN) {
+    switch (N) {
+      case 64: G(64, TEPI_LN);
+      case 128: G(128, TEPI_LN);
+      case 256: G(256, TEPI_LN);
+      case 512: G(512, TEPI_LN);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (epi == TEPI_SWIGLU) {
+    if (N % 256 == 0) G(256, TEPI_SWIGLU);
+    if (N % 128 == 0) G(128, TEPI_SWIGLU);
+    if (N % 64 == 0) G(64, TEPI_SWIGLU);
+    return cudaErrorInvalidValue;
+  }
+  if (N % 256 == 0) G(256, TEPI_STORE);
+  if (N % 128 == 0) G(128, TEPI_STORE);
+  if (N % 64 == 0) G(64, TEPI_STORE);
+  G(32, TEPI_STORE);
+#undef G
+}
+
+cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
+                    float *Cf, int64_t ldcf, cudaStream_t st) {
+  tc::EpiArgs ea{(bf16 *)Cs, ldcs, Cf, ldcf, nullptr, nullptr, 0.f};
+  return gemm_dispatch(tc::TEPI_STORE, A, lda, Bt, M, N, K, ea, st);
+}
+
+// ---- SwiGLUFFN (+LN) over rows, as two tcgen05 GEMMs with H (bf16) in a scratch buffer ----
+static void *g_hscratch = nullptr;
+static size_t g_hcap = 0;
+static std::mutex g_hmu;
+
+static cudaError_t hscratch(size_t bytes, void **out) {
+  std::lock_guard<std::mutex> lk(g_hmu);
+  if (bytes > g_hcap) {
+    if (g_hscratch) cudaFree(g_hscratch);
+    g_hscratch = nullptr;
+    g_hcap = 0;
+    cudaError_t e = cudaMalloc(&g_hscratch, bytes);
+    if (e != cudaSuccess) return e;
+    g_hcap = bytes;
+  }
+  *out = g_hscratch;
+  return cudaSuccess;
+}
+
+cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, const void *Wo, int d, int rd,
+                   const float *g, const float *b, float eps, void *out_s, int64_t ldo, float *out_f, int64_t ldof,
+                   cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  void *H = nullptr;
+  cudaError_t e = hscratch((size_t)rows * rd * 2, &H);
+  if (e != cudaSuccess) return e;
+  tc::EpiArgs e1{(bf16 *)H, rd, nullptr, 0, nullptr, nullptr, 0.f};
+  e = gemm_dispatch(tc::TEPI_SWIGLU, in, ldi, W1, rows, 2 * rd, d, e1, st);
+  if (e != cudaSuccess) return e;
+  tc::EpiArgs e2{(bf16 *)out_s, ldo, out_f, ldof, g, b, eps};
+  return gemm_dispatch(g ? tc::TEPI_LN : tc::TEPI_STORE, H, rd, Wo, rows, d, rd, e2, st);
+}
+
+}  // namespace stca
+
+// Stage-isolated test hook (not part of include/stca.h): one tcgen05 GEMM with the given
+// epilogue (0 store, 1 swiglu, 2 layernorm), so tests can compare it with a torch fp32
+// reference of the same op.
+extern "C" int stca_debug_tc_gemm(int epi, const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K,
+                                  void *Cs, int64_t ldcs, float *Cf, int64_t ldcf, const float *g, const float *b,
+                                  float eps, void *stream) {
+  stca::tc::EpiArgs ea{(stca::bf16 *)Cs, ldcs, Cf, ldcf, g, b, eps};
+  return (int)stca::gemm_dispatch(epi, A, lda, Bt, M, N, K, ea, (cudaStream_t)stream);
+}

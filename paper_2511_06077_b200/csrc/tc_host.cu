@@ -1,0 +1,83 @@
+// tc_host.cu -- weight repacks into K-major bf16 layouts for TMA/UMMA, capability check,
+// and the history projection driver of the bf16 path.
+#include <string.h>
+
+#include <vector>
+
+#include "launch.h"
+#include "tc.h"
+
+namespace stca {
+
+static __global__ void k_transpose_bf16(const bf16 *__restrict__ src, int64_t rows, int64_t cols,
+                                        bf16 *__restrict__ dst) {
+  __shared__ bf16 t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) t[i][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst [cols x rows]
+    if (r < rows && c < cols) dst[c * rows + r] = t[threadIdx.x][i];
+  }
+}
+
+static void *transpose_dev(const void *src, int64_t rows, int64_t cols, const DevAlloc &alloc) {
+  void *dst = alloc((size_t)rows * cols * 2);
+  if (!dst) return nullptr;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  note_launch();
+  k_transpose_bf16<<<grid, dim3(32, 8)>>>((const bf16 *)src, rows, cols, (bf16 *)dst);
+  if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+  return dst;
+}
+
+static uint16_t to_bf16_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+bool tc_available() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0, major = 0, minor = 0;
+    ok = cudaGetDevice(&dev) == cudaSuccess &&
+         cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess && major == 10 &&
+         minor == 0;
+    cudaGetLastError();
+  }
+  return ok == 1;
+}
+
+bool tc_prepare_ffn(const float *Wu, const float *Wv, const float *Wo, int d, int rd, TcWeights *tc,
+                    const DevAlloc &alloc) {
+  // W1^T [2rd x d], 32-row chunks interleaved: rows 64c..64c+31 = Wu[:, 32c..]^T, +32.. = Wv[:, 32c..]^T
+  std::vector<uint16_t> w1((size_t)2 * rd * d), wo((size_t)d * rd);
+  for (int c = 0; c < rd / 32; ++c)
+    for (int j = 0; j < 32; ++j)
+      for (int e = 0; e < d; ++e) {
+        w1[(size_t)(64 * c + j) * d + e] = to_bf16_bits(Wu[(size_t)e * rd + 32 * c + j]);
+        w1[(size_t)(64 * c + 32 + j) * d + e] = to_bf16_bits(Wv[(size_t)e * rd + 32 * c + j]);
+      }
+  for (int k = 0; k < rd; ++k)
+    for (int n = 0; n < d; ++n) wo[(size_t)n * rd + k] = to_bf16_bits(Wo[(size_t)k * d + n]);
+  tc->W1h = alloc(w1.size() * 2);
+  tc->Woh = alloc(wo.size() * 2);
+  if (!tc->W1h || !tc->Woh) return false;
+  return cudaMemcpy(tc->W1h, w1.data(), w1.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(tc->Woh, wo.data(), wo.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+bool tc_prepare_layer(const void *WQK, const void *WVO, const void *WC, int i, int d, int h, TcWeights *tc,
+                      const DevAlloc &alloc) {
+  if (WQK && !(tc->WQK = transpose_dev(WQK, d, (int64_t)h * d, alloc))) return false;
+  if (WVO && !(tc->WVO = transpose_dev(WVO, (int64_t)h * d, d, alloc))) return false;
+  if (WC && !(tc->WC = transpose_dev(WC, (int64_t)i * d, d, alloc))) return false;
+  return true;
+}
+
+}  // namespace stca
