@@ -736,7 +736,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     if (tc_attn) {
-      CU(stca::tc_attention(h->U.p, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+      CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     }

@@ -21,11 +21,4 @@ cudaError_t tc_project(const TcProj &p, cudaStream_t st) {
   return cudaSuccess;
 }
 
-bool tc_attention_supported(int) { return false; }
-
-cudaError_t tc_attention(const void *, const void *, int64_t, const AttnItem *, int64_t, int, void *, float *,
-                         cudaStream_t) {
-  return cudaErrorNotSupported;
-}
-
 }  // namespace stca
