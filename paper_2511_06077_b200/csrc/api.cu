@@ -89,6 +89,7 @@ struct stca_handle {
   LayerW L[STCA_MAX_LAYERS];
   void *W1z = nullptr, *Woz = nullptr, *WZ = nullptr;
   stca::TcWeights tcz;
+  stca::TcProjWeights tcp;  // all layers' history FFN/LN, concatenated for the fused projection
   // projection state
   int64_t B = -1;
   std::vector<int64_t> start, len, coff;  // start'_b (input rows), L'_b, compacted offsets [B+1]
@@ -465,6 +466,20 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
     if (h->bf16 && !stca::tc_prepare_layer(Ly.WQK, Ly.WVO, Ly.WC, i, d, hh, &Ly.tc, [&](size_t n) { return dalloc(h, n); }))
       return bad(fail(h, STCA_ERR_OOM, "tc repack failed"));
   }
+  if (h->bf16) {
+    std::vector<const float *> wu(M), wv(M), wo_(M), gg(M), bb(M);
+    for (int i = 0; i < M; ++i) {
+      std::string p = "L" + std::to_string(i + 1) + ".hist.";
+      wu[i] = W(p + "Wu");
+      wv[i] = W(p + "Wv");
+      wo_[i] = W(p + "Wo");
+      gg[i] = W(p + "ln_g");
+      bb[i] = W(p + "ln_b");
+    }
+    if (!stca::tc_prepare_proj(wu.data(), wv.data(), wo_.data(), gg.data(), bb.data(), M, d, rd, &h->tcp,
+                               [&](size_t n) { return dalloc(h, n); }))
+      return bad(fail(h, STCA_ERR_OOM, "projection weight repack failed"));
+  }
   if (cfg->with_z) {
     if (!ffn("z", &h->W1z, &h->Woz, &h->tcz)) return bad(fail(h, STCA_ERR_OOM, "upload failed (z)"));
     const float *wz = W("z.WZ");
@@ -567,6 +582,10 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     pj.eps = h->cfg.ln_eps;
     pj.out = h->xt_cache.p;
     pj.out_layer_stride = T2 * d;
+    pj.W1cat = h->tcp.W1cat;
+    pj.Wocat = h->tcp.Wocat;
+    pj.gcat = h->tcp.gcat;
+    pj.bcat = h->tcp.bcat;
     for (int i = 0; i < M; ++i) {
       pj.W1[i] = h->L[i].tc.W1h;
       pj.Wo[i] = h->L[i].tc.Woh;

@@ -30,7 +30,18 @@ struct TcProj {
   const float *g[16] = {}, *b[16] = {};
   void *out = nullptr;            // layer i at out + i * out_layer_stride elements (bf16)
   int64_t out_layer_stride = 0;
+  // fused kernel (d == 128): all layers concatenated
+  const void *W1cat = nullptr;    // [M x 2rd x d] bf16, per layer the chunk-interleaved W1^T
+  const void *Wocat = nullptr;    // [M x rd x d] bf16, row-major W_o (MN-major B operand)
+  const float *gcat = nullptr, *bcat = nullptr;  // [M x d]
 };
+
+struct TcProjWeights {
+  void *W1cat = nullptr, *Wocat = nullptr;
+  float *gcat = nullptr, *bcat = nullptr;
+};
+bool tc_prepare_proj(const float *const *Wu, const float *const *Wv, const float *const *Wo, const float *const *g,
+                     const float *const *b, int M, int d, int rd, TcProjWeights *out, const DevAlloc &alloc);
 
 bool tc_available();                       // sm_100a tensor-core path compiled in and usable
 bool tc_attention_supported(int d);

@@ -81,3 +81,34 @@ bool tc_prepare_layer(const void *WQK, const void *WVO, const void *WC, int i, i
 }
 
 }  // namespace stca
+
+namespace stca {
+
+bool tc_prepare_proj(const float *const *Wu, const float *const *Wv, const float *const *Wo, const float *const *g,
+                     const float *const *b, int M, int d, int rd, TcProjWeights *out, const DevAlloc &alloc) {
+  std::vector<uint16_t> w1((size_t)M * 2 * rd * d), wo((size_t)M * rd * d);
+  std::vector<float> gg((size_t)M * d), bb((size_t)M * d);
+  for (int i = 0; i < M; ++i) {
+    uint16_t *W1 = w1.data() + (size_t)i * 2 * rd * d, *WO = wo.data() + (size_t)i * rd * d;
+    for (int c = 0; c < rd / 32; ++c)
+      for (int j = 0; j < 32; ++j)
+        for (int e = 0; e < d; ++e) {
+          W1[(size_t)(64 * c + j) * d + e] = to_bf16_bits(Wu[i][(size_t)e * rd + 32 * c + j]);
+          W1[(size_t)(64 * c + 32 + j) * d + e] = to_bf16_bits(Wv[i][(size_t)e * rd + 32 * c + j]);
+        }
+    for (size_t k = 0; k < (size_t)rd * d; ++k) WO[k] = to_bf16_bits(Wo[i][k]);
+    memcpy(gg.data() + (size_t)i * d, g[i], sizeof(float) * d);
+    memcpy(bb.data() + (size_t)i * d, b[i], sizeof(float) * d);
+  }
+  out->W1cat = alloc(w1.size() * 2);
+  out->Wocat = alloc(wo.size() * 2);
+  out->gcat = (float *)alloc(gg.size() * 4);
+  out->bcat = (float *)alloc(bb.size() * 4);
+  if (!out->W1cat || !out->Wocat || !out->gcat || !out->bcat) return false;
+  return cudaMemcpy(out->W1cat, w1.data(), w1.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(out->Wocat, wo.data(), wo.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(out->gcat, gg.data(), gg.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(out->bcat, bb.data(), bb.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+}  // namespace stca
