@@ -17,8 +17,8 @@
 // 2^8 (exact: the final 1/l uses the same stale max).  Output: normalised Y (bf16) for
 // single-chunk requests, or (max, sum, O) fp32 partials for the split-K merge.
 //
-// Warp roles (192 threads): 0 = TMA producer, 1 = TMEM allocator + MMA issuer,
-// 2..5 = softmax / correction / epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (192 threads): 0..3 = softmax / correction / epilogue (TMEM lane quarter = warp),
+// 4 = TMA producer, 5 = TMEM allocator + MMA issuer (highest ids: the warp arbiter prefers them).
 #include <math.h>
 
 #include "launch.h"
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nt = (it.klen + AT_BN - 1) / AT_BN;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 4 && lane == 0) {
     tma_prefetch(&mapU);
     tma_prefetch(&mapX);
     mbar_init(u_full, 1);
@@ -76,14 +76,14 @@ __global__ void __launch_bounds__(192, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tslot, 512);
+  if (warp == 5) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t tS = tmem, tO = tmem + 256;  // S buffers at cols [0,128) and [128,256); O at [256,384)
 
-  if (warp == 0) {
+  if (warp == 4) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
       const uint64_t pol_x = policy_evict_first();
       mbar_expect_tx(u_full, AT_U_BYTES);
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d_hint(dst + AT_X_BYTES / 2, &mapX, &x_full[s], 64, row, pol_x);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 5) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc_s = idesc_bf16(AT_BM, AT_BN, 0);  // S = U X~^T : B K-major
       constexpr uint32_t idesc_o = idesc_bf16(AT_BM, AT_D, 1);   // O += P X~  : B MN-major
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 5) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace tc

@@ -2,9 +2,9 @@
 //
 //   C[M x N] = A[M x K] . Bt^T,   A bf16 row-major (lda), Bt = B^T bf16 [N x K] (K-major)
 //
-// Warp 0: TMA producer (SWIZZLE_128B boxes of 64 K-elements), warp 1: TMEM allocator +
-// single-thread tcgen05.mma issuer (M = 128, N-slices <= 256, K = 16 per instruction),
-// warps 2-5: epilogue, one thread per accumulator row (TMEM lane), reading the fp32
+// Warps 0-3: epilogue; warp 4: TMA producer (SWIZZLE_128B boxes of 64 K-elements); warp 5: TMEM
+// allocator + single-thread tcgen05.mma issuer (M = 128, N-slices <= 256, K = 16 per instruction;
+// highest warp ids so the arbiter never starves the issuing thread).  Epilogue: one thread per accumulator row (TMEM lane), reading the fp32
 // accumulator with tcgen05.ld.  Epilogues:
 //   TEPI_STORE  : alpha*acc -> bf16 (Cs) and/or fp32 (Cf)
 //   TEPI_SWIGLU : Bt rows chunk-interleaved [u_32c..u_32c+31 | v_32c..v_32c+31]:
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(192, 1)
   const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
   const int nk = (K + C::BK - 1) / C::BK;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 4 && lane == 0) {
     tma_prefetch(&mapA);
     tma_prefetch(&mapB);
     for (int s = 0; s < C::STAGES; ++s) {
@@ -79,13 +79,13 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(tfull, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  if (warp == 5) tmem_alloc(tslot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  if (warp == 0) {
+  if (warp == 4) {
     if (lane == 0) {  // TMA producer
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < BN / C::NS; ++j) tma_load_2d(sb + j * C::NS * 128, &mapB, &full[s], kb * C::BK, n0 + j * C::NS);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 5) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = idesc_bf16(128, C::NS, 0);
       for (int kb = 0; kb < nk; ++kb) {
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       umma_commit(tfull);
     }
-  } else {  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+  } else {  // epilogue warps 0..3: TMEM lane quarter = warp
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int64_t grow = (int64_t)m0 + row;
@@ -226,8 +226,11 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == 5) tmem_dealloc(tmem, C::TMEM_COLS);
 }
+
+// bf16 [n2 x n1 x n0] (n0 innermost, contiguous), box = box1 rows x 64 x 1, SWIZZLE_128B
+bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1);
 
 // ---------------------------------------------------------------------------
 // host side
@@ -254,6 +257,19 @@ bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, 
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)n0, (cuuint64_t)n1, (cuuint64_t)n2};
+  cuuint64_t gstride[2] = {(cuuint64_t)(n0 * 2), (cuuint64_t)(n1 * n0 * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), gdim, gstride, box, estride,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
