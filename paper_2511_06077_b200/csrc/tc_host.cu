@@ -90,11 +90,12 @@ bool tc_prepare_proj(const float *const *Wu, const float *const *Wv, const float
   std::vector<float> gg((size_t)M * d), bb((size_t)M * d);
   for (int i = 0; i < M; ++i) {
     uint16_t *W1 = w1.data() + (size_t)i * 2 * rd * d, *WO = wo.data() + (size_t)i * rd * d;
-    for (int c = 0; c < rd / 32; ++c)
-      for (int j = 0; j < 32; ++j)
+    // fused projection: 64-column chunks, rows 128c..128c+63 = Wu[:, 64c..]^T, +64.. = Wv[:, 64c..]^T
+    for (int c = 0; c < rd / 64; ++c)
+      for (int j = 0; j < 64; ++j)
         for (int e = 0; e < d; ++e) {
-          W1[(size_t)(64 * c + j) * d + e] = to_bf16_bits(Wu[i][(size_t)e * rd + 32 * c + j]);
-          W1[(size_t)(64 * c + 32 + j) * d + e] = to_bf16_bits(Wv[i][(size_t)e * rd + 32 * c + j]);
+          W1[(size_t)(128 * c + j) * d + e] = to_bf16_bits(Wu[i][(size_t)e * rd + 64 * c + j]);
+          W1[(size_t)(128 * c + 64 + j) * d + e] = to_bf16_bits(Wv[i][(size_t)e * rd + 64 * c + j]);
         }
     for (size_t k = 0; k < (size_t)rd * d; ++k) WO[k] = to_bf16_bits(Wo[i][k]);
     memcpy(gg.data() + (size_t)i * d, g[i], sizeof(float) * d);
