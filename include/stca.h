@@ -140,6 +140,10 @@ int32_t stca_plan_chunks(int64_t L, int32_t chunk_keys, int64_t *chunk_len);
 int64_t stca_plan_attention(const int64_t *hist_len, const int64_t *tgt_off, int64_t B, int32_t h,
                             int32_t qtile, int32_t chunk_keys, int64_t *items, int64_t cap);
 
+/* Split-history ownership: rank g of G owns the contiguous key range [*own0, *own0 + *olen) of a
+ * history of L keys -- the chunks c with floor(c G / C) == g of its stca_plan_chunks plan. */
+void stca_plan_split(int64_t L, int32_t chunk_keys, int32_t G, int32_t g, int64_t *own0, int64_t *olen);
+
 /* LPT partition of requests over n_parts GPUs by cost (descending cost to the
  * least-loaded part, ties to the lowest index; exact integer arithmetic).
  * part_out[b] in [0, n_parts). */

@@ -19,10 +19,11 @@ from typing import Dict, Optional
 import numpy as np
 
 from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_shards,  # noqa: F401
-                   plan_suffix, status_string, validate_offsets, EXCHANGE_FN, _Config, _Tensor, LIB_PATH)
+                   plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, _Config,
+                   _Tensor, LIB_PATH)
 
-__all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_shards", "plan_suffix",
-           "validate_offsets", "status_string", "LIB_PATH"]
+__all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_shards", "plan_split", "plan_suffix",
+           "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange"]
 
 
 def _ptr(x) -> int:
@@ -135,3 +136,73 @@ class STCA:
                                        off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
                                        ctypes.c_void_p(_ptr(out_Z)), ctypes.c_void_p(_ptr(out_z)),
                                        ctypes.c_void_p(_stream(stream))))
+
+
+# ---------------------------------------------------------------------------
+# split-history exchange callbacks (stca_exchange_fn): an all-gather of raw device bytes
+# ---------------------------------------------------------------------------
+class _DevBytes:
+    """Zero-copy view of `n` device bytes at `ptr` (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def _torch_stream(stream: int):
+    import torch
+    return torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+
+
+def nccl_exchange(group=None):
+    """Exchange over torch.distributed (backend "nccl"): all_gather_into_tensor, ordered on the
+    library's stream.  Pass as STCA(..., split_world=W, split_rank=r, exchange=nccl_exchange())."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+
+    def fn(ctx, send, recv, nbytes, stream):
+        try:
+            s = torch.as_tensor(_DevBytes(send, nbytes), device="cuda")
+            r = torch.as_tensor(_DevBytes(recv, nbytes * world), device="cuda")
+            with torch.cuda.stream(_torch_stream(stream)):
+                dist.all_gather_into_tensor(r, s, group=group)
+            return 0
+        except Exception:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
+            return 1
+    return fn
+
+
+class ThreadExchange:
+    """G split-history ranks as host threads sharing one device (tests / emulation): the
+    all-gather is done with device-to-device copies between the ranks' buffers."""
+
+    def __init__(self, G: int):
+        import threading
+        self.G = G
+        self.barrier = threading.Barrier(G)
+        self.sends = [None] * G
+
+    def for_rank(self, rank: int):
+        import torch
+
+        def fn(ctx, send, recv, nbytes, stream):
+            try:
+                st = _torch_stream(stream)
+                st.synchronize()                      # this rank's partials are complete
+                self.sends[rank] = (send, nbytes)
+                self.barrier.wait()
+                r = torch.as_tensor(_DevBytes(recv, nbytes * self.G), device="cuda")
+                with torch.cuda.stream(st):
+                    for g, (p, n) in enumerate(self.sends):
+                        r[g * n:(g + 1) * n].copy_(torch.as_tensor(_DevBytes(p, n), device="cuda"))
+                st.synchronize()
+                self.barrier.wait()                   # every rank has read every send buffer
+                return 0
+            except Exception:  # pragma: no cover
+                import traceback
+                traceback.print_exc()
+                return 1
+        return fn

@@ -37,7 +37,8 @@ _I64P = ctypes.POINTER(ctypes.c_int64)
 
 SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy", "stca_last_error",
            "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
-           "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches"]
+           "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
+           "stca_plan_split"]
 
 
 def lib():
@@ -76,6 +77,8 @@ def lib():
         L.stca_plan_attention.restype = ctypes.c_int64
         L.stca_plan_shards.argtypes = [_I64P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
         L.stca_plan_shards.restype = None
+        L.stca_plan_split.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I64P, _I64P]
+        L.stca_plan_split.restype = None
         _lib = L
     return _lib
 
@@ -134,3 +137,10 @@ def plan_shards(cost, n_parts: int) -> np.ndarray:
 def kernel_launches() -> int:
     """Process-wide number of kernels libstca has launched (bench: gpu_launches)."""
     return int(lib().stca_kernel_launches())
+
+
+def plan_split(L: int, chunk_keys: int, G: int, g: int):
+    """(own0, olen): the key range rank g of G owns in split-history mode."""
+    a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+    lib().stca_plan_split(L, chunk_keys, G, g, ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value

@@ -93,11 +93,12 @@ struct stca_handle {
   // projection state
   int64_t B = -1;
   std::vector<int64_t> start, len, coff;  // start'_b (input rows), L'_b, compacted offsets [B+1]
+  std::vector<int64_t> own0, olen;         // split-history: first owned key and owned key count (else 0, L'_b)
   int64_t T2 = 0;
   DevBuf xt_cache;  // M x [T2 x d] storage
   DevBuf xin, xgather, seg, proj_h, proj_y;
   // forward scratch
-  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, items, mitems, zout, Zout;
+  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, zout, Zout;
   HostPinned pin;
   int64_t chunk_cap = 4096;
 };
@@ -239,6 +240,15 @@ int64_t stca_plan_attention(const int64_t *hist_len, const int64_t *tgt_off, int
       o[0] = v[i].b; o[1] = v[i].q0; o[2] = v[i].nq; o[3] = v[i].k0; o[4] = v[i].kl; o[5] = v[i].c;
     }
   return n;
+}
+
+void stca_plan_split(int64_t L, int32_t chunk_keys, int32_t G, int32_t g, int64_t *own0, int64_t *olen) {
+  int64_t cl = 0;
+  const int64_t C = stca_plan_chunks(L, chunk_keys, &cl);
+  if (G < 1) G = 1;
+  const int64_t c0 = ((int64_t)g * C + G - 1) / G, c1 = ((int64_t)(g + 1) * C + G - 1) / G;
+  *own0 = std::min(L, c0 * cl);
+  *olen = std::min(L, c1 * cl) - *own0;
 }
 
 void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *part_out) {
@@ -503,7 +513,7 @@ extern "C" void stca_destroy(stca_handle *h) {
   for (void *p : h->allocs) cudaFree(p);
   DevBuf *bufs[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,   &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,  &h->ybuf32, &h->U,      &h->Y,
-                    &h->part,     &h->items, &h->mitems, &h->zout,  &h->Zout};
+                    &h->part,     &h->partg, &h->items, &h->mitems, &h->zout,  &h->Zout};
   for (DevBuf *b : bufs) b->release();
   h->pin.release();
   cudaGetLastError();
@@ -535,30 +545,34 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
   h->start.assign(B, 0);
   stca_plan_suffix(hist_off, B, h->cfg.L_infer, h->start.data());
   h->len.assign(B, 0);
+  h->own0.assign(B, 0);
+  h->olen.assign(B, 0);
   h->coff.assign(B + 1, 0);
-  bool truncated = false;
+  bool gather = false;
+  const int G = h->cfg.split_world, g = h->cfg.split_rank;
   for (int64_t b = 0; b < B; ++b) {
     h->len[b] = hist_off[b + 1] - h->start[b];
-    h->coff[b + 1] = h->coff[b] + h->len[b];
-    truncated |= h->start[b] != hist_off[b];
+    h->olen[b] = h->len[b];
+    if (G > 1)  // split-history: this rank owns chunks [ceil(g C / G), ceil((g+1) C / G)) of the history
+      stca_plan_split(h->len[b], (int32_t)h->chunk_cap, G, g, &h->own0[b], &h->olen[b]);
+    h->coff[b + 1] = h->coff[b] + h->olen[b];
+    gather |= h->start[b] + h->own0[b] != hist_off[b] || h->olen[b] != hist_off[b + 1] - hist_off[b];
   }
-  const int64_t T2 = h->coff[B];
-  // split-history: this rank projects only its own chunks -- handled by restricting rows in attention;
-  // the projection covers all rows (token-wise, cheap relative to replication of inputs).
+  const int64_t T2 = h->coff[B];  // rows of the X~ cache (the suffix rows this rank owns)
   const void *Xd = X;
   if (T > 0 && !is_device_ptr(X)) {  // host input: stage H2D on the stream
     CU(h->xin.ensure((size_t)T * row_bytes));
     CU(cudaMemcpyAsync(h->xin.p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
     Xd = h->xin.p;
   }
-  if (truncated) {  // gather the suffixes into a compacted buffer
+  if (gather && T2 > 0) {  // gather the (owned) suffix rows into a compacted buffer
     std::vector<int64_t> seg;
     int64_t maxlen = 0;
     for (int64_t b = 0; b < B; ++b) {
-      seg.push_back(h->start[b]);
+      seg.push_back(h->start[b] + h->own0[b]);
       seg.push_back(h->coff[b]);
-      seg.push_back(h->len[b]);
-      maxlen = std::max(maxlen, h->len[b]);
+      seg.push_back(h->olen[b]);
+      maxlen = std::max(maxlen, h->olen[b]);
     }
     CU(h->seg.ensure(seg.size() * 8));
     CU(h->pin.ensure(seg.size() * 8));
@@ -710,23 +724,30 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   std::vector<stca::MergeItem> mi;
   int64_t part_rows = 0;
   int max_rows = 0;
+  const int G = h->cfg.split_world, grank = h->cfg.split_rank;
   for (int64_t b = 0; b < B; ++b) {
     const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
     const int32_t nc = stca_plan_chunks(h->len[b], (int32_t)h->chunk_cap, nullptr);
-    if (rows == 0 || nc <= 1) continue;
+    if (rows == 0 || (nc <= 1 && G == 1)) continue;  // split-history: every request goes through the merge
     part_base[b] = part_rows;
     mi.push_back({tgt_off[b] * hh, part_rows, (int32_t)rows, nc});
     part_rows += rows * nc;
     max_rows = std::max<int>(max_rows, (int)rows);
   }
-  std::vector<stca::AttnItem> items((size_t)nit);
+  std::vector<stca::AttnItem> items;
+  items.reserve((size_t)nit);
   for (int64_t i = 0; i < nit; ++i) {
     const int64_t *o = &it6[6 * i];
     const int64_t b = o[0];
-    stca::AttnItem &a = items[i];
+    if (G > 1) {  // split-history: only the chunks this rank owns (floor(c G / C) == rank)
+      const int32_t nc = stca_plan_chunks(h->len[b], (int32_t)h->chunk_cap, nullptr);
+      if ((o[5] * G) / nc != grank) continue;
+    }
+    items.emplace_back();
+    stca::AttnItem &a = items.back();
     a.qrow0 = o[1];
     a.nq = (int32_t)o[2];
-    a.key0 = h->coff[b] + o[3];
+    a.key0 = h->coff[b] + (o[3] - h->own0[b]);
     a.klen = (int32_t)o[4];
     a.chunk = (int32_t)o[5];
     a.pad = 0;
@@ -741,7 +762,10 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   memcpy((uint8_t *)h->pin.p + items_bytes, mi.data(), mi_bytes);
   if (items_bytes) CU(cudaMemcpyAsync(h->items.p, h->pin.p, items_bytes, cudaMemcpyHostToDevice, st));
   if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, (uint8_t *)h->pin.p + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
-  if (part_rows) CU(h->part.ensure((size_t)part_rows * (d + 2) * 4));
+  nit = (int64_t)items.size();
+  const size_t part_bytes = (size_t)part_rows * (d + 2) * 4;
+  if (part_rows) CU(h->part.ensure(part_bytes));
+  if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G));
 
   // a2: q(1) = LN(SwiGLUFFN(1)(x_t)), Eq.(3)
   LayerW &L1 = h->L[0];
@@ -759,8 +783,14 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     }
-    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows,
-                            h->part.as<float>(), d, h->Y.p, st));
+    const float *merged_from = h->part.as<float>();
+    if (G > 1 && part_rows) {  // split-history exchange: all-gather every rank's partials (one step per layer)
+      if (h->cfg.exchange(h->cfg.exchange_ctx, h->part.p, h->partg.p, part_bytes, (void *)st) != 0)
+        return fail(h, STCA_ERR_COMM, "split-history exchange failed at layer %d", i);
+      merged_from = h->partg.as<float>();
+    }
+    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, merged_from, d,
+                            G, (int64_t)(part_bytes / 4), h->Y.p, st));
     // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
     s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,
              Zd + (size_t)(i - 1) * d, (int64_t)M * d, Nt, d, hh * d, st);

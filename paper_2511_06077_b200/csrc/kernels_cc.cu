@@ -229,37 +229,41 @@ cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const Attn
 // --------------------------------------------------------------------------
 // split-K LSE merge (K-E): fold chunks 0..C-1 in order, per query row
 //   mu* = max_c mu_c; l* = sum_c 2^(mu_c - mu*) l_c; Y = sum_c 2^(mu_c - mu*) O_c / l*
+// In split-history mode (G > 1) `part` holds every rank's partial buffer (rank-major, stride
+// rank_stride floats) and chunk c of a request with C chunks is read from its owner rank
+// floor(c G / C); with G = 1 this is the intra-GPU split-K merge.
 // grid: (items, row blocks of 8 rows), warp per row.
 // --------------------------------------------------------------------------
 template <typename S>
-__global__ void k_merge(const MergeItem *__restrict__ items, const float *__restrict__ part, int d,
-                        S *__restrict__ Y) {
+__global__ void k_merge(const MergeItem *__restrict__ items, const float *__restrict__ part, int d, int G,
+                        int64_t rank_stride, S *__restrict__ Y) {
   const MergeItem it = items[blockIdx.x];
   const int q = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (q >= it.rows) return;
   const int64_t stride = (int64_t)it.rows * (d + 2);
   const float *p0 = part + (it.part_row + q) * (int64_t)(d + 2);
+  auto P = [&](int c) { return p0 + (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride; };
   float mu = -INFINITY;
-  for (int c = 0; c < it.nchunks; ++c) mu = fmaxf(mu, p0[c * stride]);
+  for (int c = 0; c < it.nchunks; ++c) mu = fmaxf(mu, P(c)[0]);
   float l = 0.f;
-  for (int c = 0; c < it.nchunks; ++c) l += exp2f(p0[c * stride] - mu) * p0[c * stride + 1];
+  for (int c = 0; c < it.nchunks; ++c) l += exp2f(P(c)[0] - mu) * P(c)[1];
   const float inv = 1.f / l;
   for (int e = lane; e < d; e += 32) {
     float acc = 0.f;
-    for (int c = 0; c < it.nchunks; ++c) acc += exp2f(p0[c * stride] - mu) * p0[c * stride + 2 + e];
+    for (int c = 0; c < it.nchunks; ++c) acc += exp2f(P(c)[0] - mu) * P(c)[2 + e];
     Y[(it.qrow0 + q) * d + e] = from_f<S>(acc * inv);
   }
 }
 
 cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
-                           int d, void *Y, cudaStream_t st) {
+                           int d, int G, int64_t rank_stride, void *Y, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   dim3 grid((unsigned)n_items, (unsigned)((max_rows + 7) / 8));
   note_launch();
   if (is_bf16)
-    k_merge<bf16><<<grid, 256, 0, st>>>(items, part, d, (bf16 *)Y);
+    k_merge<bf16><<<grid, 256, 0, st>>>(items, part, d, G, rank_stride, (bf16 *)Y);
   else
-    k_merge<float><<<grid, 256, 0, st>>>(items, part, d, (float *)Y);
+    k_merge<float><<<grid, 256, 0, st>>>(items, part, d, G, rank_stride, (float *)Y);
   return cudaGetLastError();
 }
 

@@ -131,3 +131,21 @@ def test_lpt_shards_match_reference():
             got = stca.plan_shards(cost, P)
             assert got.tolist() == lpt_reference(cost.tolist(), P)
             assert set(got.tolist()) <= set(range(P))
+
+
+@pytest.mark.parametrize("cap", [128, 1280, 4096])
+def test_split_history_ownership_partitions_keys(cap):
+    """Split-history (PAR3): ranks own contiguous, disjoint, whole-chunk key ranges covering [0, L)."""
+    for L in [1, 100, 1280, 1281, 4097, 10000, 12345]:
+        n, cl = stca.plan_chunks(L, cap)
+        for G in range(1, 10):
+            pos = 0
+            for g in range(G):
+                o0, ol = stca.plan_split(L, cap, G, g)
+                assert o0 == pos and ol >= 0
+                assert o0 % cl == 0 or ol == 0
+                # every owned chunk c satisfies floor(c G / C) == g (the merge kernel's owner rule)
+                for c in range(o0 // cl, (o0 + ol + cl - 1) // cl if ol else o0 // cl):
+                    assert (c * G) // n == g
+                pos += ol
+            assert pos == L
