@@ -536,6 +536,13 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
                                 (long long)badi, (long long)hist_off[0], (long long)hist_off[B], (long long)T);
   s = check_offsets(hist_off, B, T, true, &badi);
   if (s != STCA_OK) return fail(h, s, "empty history for request %lld", (long long)badi);
+  for (int64_t b = 0; b < B; ++b) {  // the split-K merge folds at most 8 chunks per history
+    int64_t Lb = hist_off[b + 1] - hist_off[b];
+    if (h->cfg.L_infer > 0 && Lb > h->cfg.L_infer) Lb = h->cfg.L_infer;
+    if (stca_plan_chunks(Lb, (int32_t)h->chunk_cap, nullptr) > 8)
+      return fail(h, STCA_ERR_UNSUPPORTED, "history %lld has %lld keys > 8 x chunk_keys (%lld); raise chunk_keys",
+                  (long long)b, (long long)Lb, (long long)h->chunk_cap);
+  }
   CU(cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
   const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
