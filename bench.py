@@ -17,12 +17,9 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -157,7 +154,9 @@ def config_dict(wl, args):
     L = wl.lengths
     return {"workload": c.name, "requests": int(len(L)), "targets_per_request": int(np.diff(wl.tgt_off)[0]),
             "L_avg": float(L.mean()), "L_max": int(L.max()), "L_infer": c.L_infer, "d": c.d, "h": c.h, "r": c.r,
-            "M": c.M, "T": wl.T, "N_t": wl.Nt, "parallelism": f"requests sharded over {args.gpus} GPU(s), weak",
+            "M": c.M, "T": wl.T, "N_t": wl.Nt,
+            "parallelism": (f"split-history over {args.gpus} GPU(s) (NCCL all-gather of partials per layer)"
+                            if c.name == "split1" else f"requests sharded over {args.gpus} GPU(s), weak"),
             "l2": "inputs larger than L2 (X and the X~ cache exceed 126 MB); no flush", "seed": args.seed}
 
 
@@ -190,12 +189,17 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = workload.make_workload(args.config, seed=args.seed + 1000 * rank)   # this rank's shard (weak scaling)
+    # split1 (BASELINE config 5): ONE L = 10k history split over the ranks (split-history, strong
+    # scaling, one all-gather of partials per layer); every other config: each rank its own shard
+    split = args.config == "split1"
+    wl = workload.make_workload(args.config, seed=args.seed if split else args.seed + 1000 * rank)
     c = wl.cfg
     W = workload.full_weights(workload.make_workload(args.config, seed=args.seed, B=1)) if rank else \
         workload.full_weights(wl)                                            # weights replicated (seed 0 draw)
     model = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, dtype=c.dtype, with_z=c.with_z,
-                      device=local)
+                      device=local, chunk_keys=1280 if split else 0,
+                      split_rank=rank if split else 0, split_world=world if split else 1,
+                      exchange=stca.nccl_exchange() if split and world > 1 else None)
     bf16 = c.dtype == "bf16"
     Xh = wl.X_bits.view(np.int16) if bf16 else wl.X
     xth = wl.xt_bits.view(np.int16) if bf16 else wl.xt
@@ -242,7 +246,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, fwd_max = float(t[0]), float(t[1])
-    total_targets = wl.Nt * world
+    total_targets = wl.Nt if split else wl.Nt * world
     value = total_targets / (ms_max * 1e-3)
 
     # e2e through the C ABI with HOST buffers (pinned), H2D/D2H inside the timed region
@@ -283,7 +287,8 @@ def main():
             traffic = json.load(open(tf)).get(c.name, {}).get("projection_dram_bytes_per_launch")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if split else "weak",
+            "vs_baseline": None,
             "dtype": "bf16" if bf16 else "fp32", "data": "synthetic", "config": config_dict(wl, args),
             "roofline": {"kernel": "history projection (a1, stca_project_history)", "bound": "tensor",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

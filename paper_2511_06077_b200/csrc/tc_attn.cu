@@ -1,25 +1,32 @@
-// tc_attn.cu -- fused ragged single-query cross attention on tcgen05 (sm_100a).
+// tc_attn.cu -- fused ragged single-query cross attention on tcgen05 (sm_100a), SURVEY §2.2 K-C.
 //
 // PAPER.md Eq.(13): per head r, u = (q W_Q^r) W_K^r^T, alpha = softmax(u X~^T /
-// sqrt(d_h)), y = alpha X~.  Under RLB every target-head pair (t, r) of one
-// request is one query row u_{t,r} (pre-scaled by log2(e)/sqrt(d_h)) against the SAME
-// history rows X~_b, so a request's m_b*h query rows form the M side of two real MMAs:
+// sqrt(d_h)), y = alpha X~.  Under RLB every target-head pair (t, r) of one request
+// is one query row u_{t,r} (pre-scaled by log2(e)/sqrt(d_h)) against the SAME history rows X~_b,
+// so a request's m_b*h query rows form the M side of two real MMAs:
 //     S = U_b X~_b^T   (M = 128 query rows, N = 128 keys, K = d)
 //     O += P X~_b      (M = 128, N = d, K = 128 keys)
-// Ragged Target Attention: keys are the flattened [T' x d] cache; a work item
-// covers one request's key chunk, keys past the chunk end are masked to -inf (P = 0).
+// Ragged Target Attention: keys are the flattened [T' x d] cache; a work item covers
+// one request's key chunk, keys past the chunk end are masked to -inf (P = 0).
 //
-// One SMEM copy of each X~ tile (TMA, SWIZZLE_128B, two 64-column boxes) is read by the
-// first MMA as a K-major B operand and by the second as an MN-major B operand.  S is
-// double-buffered in TMEM, O lives in TMEM; the softmax warps (one thread per query row)
-// keep the running max / sum in fp32 registers, write P (bf16) into SMEM in the UMMA
-// K-major SW128 layout, and rescale O only when the running max grows by more than
-// 2^8 (exact: the final 1/l uses the same stale max).  Output: normalised Y (bf16) for
-// single-chunk requests, or (max, sum, O) fp32 partials for the split-K merge.
+// Operands: U and P live in TENSOR MEMORY and are the A operands of both MMAs (TS form); P is
+// written by the softmax warps as packed bf16 over the first half of the very S columns it was
+// computed from.  X~ tiles arrive by TMA (two 64-column SW128 boxes, 4-stage ring) and ONE shared
+// memory copy is read as the K-major B of S and as the MN-major B of PV, so per 128-key tile the
+// SMEM port carries only 3 x 32 KB (TMA write, two B reads).  S is double-buffered in TMEM, O
+// lives in TMEM (S 2x128 + O 128 + U 64 = 448 columns).  The softmax keeps max / sum in fp32
+// registers and rescales O only when a row max grows by more than 2^8 (exact: the final 1/l uses
+// the same stale max), warp-uniformly (tcgen05.ld/st are .sync.aligned).  Output: normalised Y
+// (bf16) for single-chunk requests, else (max, sum, O) fp32 partials for the split-K merge.
 //
-// Warp roles (192 threads): 0..3 = softmax / correction / epilogue (TMEM lane quarter = warp),
-// 4 = TMA producer, 5 = TMEM allocator + MMA issuer (highest ids: the warp arbiter prefers them).
+// Warp roles (32 (4 NP + 3) threads, NP = 2): 0..4NP-1 softmax / correction / epilogue (TMEM lane
+// quarter = warp % 4, key-column part = warp / 4: NP threads per query row exchange their maxima
+// through shared memory), then the TMA producer, the TMEM allocator + S issuer and the PV issuer.  Issuers get the highest warp ids
+// (the SM's arbiter prefers them) and S / PV are issued from different warps so that one warp's
+// mbarrier waits are covered by the other's queued MMAs.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "launch.h"
 #include "tc.h"
@@ -30,226 +37,285 @@ namespace tc {
 
 bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 
-constexpr int AT_BM = 128;       // query rows per CTA
-constexpr int AT_BN = 128;       // keys per tile
-constexpr int AT_D = 128;        // head-input width d (= row width of X~)
-constexpr int AT_STAGES = 3;     // X~ tile ring
-constexpr int AT_U_BYTES = AT_BM * AT_D * 2;   // 32 KB
+constexpr int AT_BM = 128;                     // query rows per CTA
+constexpr int AT_BN = 128;                     // keys per tile
+constexpr int AT_D = 128;                      // head-input width d (= row width of X~)
+constexpr int AT_STAGES = 4;                   // X~ tile ring
 constexpr int AT_X_BYTES = AT_BN * AT_D * 2;   // 32 KB
-constexpr int AT_P_BYTES = AT_BM * AT_BN * 2;  // 32 KB
-constexpr int AT_SMEM = 1024 + AT_U_BYTES + AT_STAGES * AT_X_BYTES + 2 * AT_P_BYTES + 256;
+constexpr int AT_NP = 2;                       // key-column parts per query row (threads per row)
+constexpr int AT_CW = AT_BN / AT_NP;            // key columns (and O columns) per softmax thread
+constexpr int AT_NSW = 4 * AT_NP;               // softmax warps
+constexpr int AT_SMEM = 1024 + AT_STAGES * AT_X_BYTES + 2 * AT_NP * 128 * 4 + AT_NP * 128 * 4 + 256;
 constexpr float AT_RESCALE_THRESHOLD = 8.f;    // log2(256)
+constexpr int AT_WP = AT_NSW, AT_WS = AT_NSW + 1, AT_WO = AT_NSW + 2, AT_THREADS = 32 * (AT_NSW + 3);
+constexpr uint32_t AT_TS = 0, AT_TO = 256, AT_TU = 384;  // TMEM columns: S0 | S1 | O | U
 
-__global__ void __launch_bounds__(192, 1)
-    k_tc_attention(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapX,
-                   const AttnItem *__restrict__ items, bf16 *__restrict__ Y, float *__restrict__ part) {
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    k_tc_attention(const __grid_constant__ CUtensorMap mapX, const bf16 *__restrict__ U, int64_t NQ,
+                   const AttnItem *__restrict__ items, bf16 *__restrict__ Y, float *__restrict__ part,
+                   unsigned long long *trace) {
+#define AT_TR(slot)                                                 \
+  do {                                                              \
+    if (trace && blockIdx.x == 0) trace[(slot)] = clock64();        \
+  } while (0)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t *sU = smem;
-  uint8_t *sX = sU + AT_U_BYTES;
-  uint8_t *sP = sX + AT_STAGES * AT_X_BYTES;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * AT_P_BYTES);
-  uint64_t *u_full = bar;                  // 1
-  uint64_t *x_full = bar + 1;              // AT_STAGES
-  uint64_t *x_empty = x_full + AT_STAGES;  // AT_STAGES
-  uint64_t *s_full = x_empty + AT_STAGES;  // 2
-  uint64_t *p_full = s_full + 2;           // 2
-  uint64_t *pv_done = p_full + 2;          // 2
+  uint8_t *sX = smem;
+  float *sMax = reinterpret_cast<float *>(sX + AT_STAGES * AT_X_BYTES);  // [tile parity][half][row]
+  float *sSum = sMax + 2 * AT_NP * 128;                                  // [part][row]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sSum + AT_NP * 128);
+  uint64_t *u_full = bar;                  // 8 warp arrivals (U written into TMEM)
+  uint64_t *x_full = bar + 1;              // AT_STAGES (TMA tx)
+  uint64_t *x_empty = x_full + AT_STAGES;  // AT_STAGES (PV of the tile done)
+  uint64_t *s_full = x_empty + AT_STAGES;  // 2 (S MMA done)
+  uint64_t *p_full = s_full + 2;           // 2 (8 warp arrivals: P written into TMEM)
+  uint64_t *pv_done = p_full + 2;          // 2 (PV MMA done: P / S buffer free, O stable)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(pv_done + 2);
 
   const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nt = (it.klen + AT_BN - 1) / AT_BN;
 
-  if (warp == 4 && lane == 0) {
-    tma_prefetch(&mapU);
+  if (warp == AT_WP && lane == 0) {
     tma_prefetch(&mapX);
-    mbar_init(u_full, 1);
+    mbar_init(u_full, AT_NSW);
     for (int s = 0; s < AT_STAGES; ++s) {
       mbar_init(&x_full[s], 1);
       mbar_init(&x_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
+      mbar_init(&p_full[b], AT_NSW);
       mbar_init(&pv_done[b], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tslot, 512);
+  if (warp == AT_WS) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 256;  // S buffers at cols [0,128) and [128,256); O at [256,384)
 
-  if (warp == 4) {
+  if (warp == AT_WP) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
       const uint64_t pol_x = policy_evict_first();
-      mbar_expect_tx(u_full, AT_U_BYTES);
-      tma_load_2d(sU, &mapU, u_full, 0, (int32_t)it.qrow0);
-      tma_load_2d(sU + AT_U_BYTES / 2, &mapU, u_full, 64, (int32_t)it.qrow0);
+      int s = 0, ph = 0;
       for (int j = 0; j < nt; ++j) {
-        const int s = j % AT_STAGES;
-        mbar_wait(&x_empty[s], ((j / AT_STAGES) & 1) ^ 1);
+        mbar_wait(&x_empty[s], ph ^ 1);
+        AT_TR(j * 16 + 0);
         uint8_t *dst = sX + s * AT_X_BYTES;
         const int32_t row = (int32_t)(it.key0 + (int64_t)j * AT_BN);
         mbar_expect_tx(&x_full[s], AT_X_BYTES);
         tma_load_2d_hint(dst, &mapX, &x_full[s], 0, row, pol_x);
         tma_load_2d_hint(dst + AT_X_BYTES / 2, &mapX, &x_full[s], 64, row, pol_x);
+        if (++s == AT_STAGES) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 5) {
-    if (lane == 0) {  // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc_s = idesc_bf16(AT_BM, AT_BN, 0);  // S = U X~^T : B K-major
-      constexpr uint32_t idesc_o = idesc_bf16(AT_BM, AT_D, 1);   // O += P X~  : B MN-major
-      const uint32_t aU = smem_u32(sU), aX = smem_u32(sX), aP = smem_u32(sP);
+  } else if (warp == AT_WS) {
+    if (lane == 0) {  // ---------------- S issuer: S_j = U X~_j^T ----------------
+      constexpr uint32_t idesc_s = idesc_bf16(AT_BM, AT_BN, 0);  // B K-major
+      const uint32_t aX = smem_u32(sX);
       mbar_wait(u_full, 0);
-      auto pv = [&](int j) {  // O += P_j X~_j
-        const int s = j % AT_STAGES, b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t xs = aX + s * AT_X_BYTES, ps = aP + b * AT_P_BYTES;
-#pragma unroll
-        for (int k = 0; k < AT_BN / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(ps + (k >> 2) * (AT_P_BYTES / 2) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(xs + k * 2048, AT_X_BYTES / 2, 1024);  // MN-major: LBO = 64-col box
-          umma_f16_ss(tO, ad, bd, idesc_o, (j | k) != 0);
-        }
-        umma_commit(&pv_done[b]);
-        umma_commit(&x_empty[s]);
-      };
+      int s = 0, ph = 0;
       for (int j = 0; j < nt; ++j) {
-        const int s = j % AT_STAGES, b = j & 1;
-        mbar_wait(&x_full[s], (j / AT_STAGES) & 1);
-        if (j >= 2) mbar_wait(&p_full[b], ((j - 2) >> 1) & 1);  // S buffer b consumed by softmax
+        const int b = j & 1;
+        mbar_wait(&x_full[s], ph);
+        AT_TR(j * 16 + 1);
+        if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // PV_{j-2} has read P from S buffer b
+        AT_TR(j * 16 + 2);
         tc_fence_after();
         const uint32_t xs = aX + s * AT_X_BYTES;
 #pragma unroll
-        for (int k = 0; k < AT_D / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(aU + (k >> 2) * (AT_U_BYTES / 2) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(xs + (k >> 2) * (AT_X_BYTES / 2) + (k & 3) * 32, 16, 1024);
-          umma_f16_ss(tS + b * AT_BN, ad, bd, idesc_s, k != 0);
-        }
+        for (int k = 0; k < AT_D / 16; ++k)
+          umma_f16_ts(tmem + AT_TS + b * AT_BN, tmem + AT_TU + k * 8,
+                      sdesc_sw128(xs + (k >> 2) * (AT_X_BYTES / 2) + (k & 3) * 32, 16, 1024), idesc_s, k != 0);
         umma_commit(&s_full[b]);
-        if (j >= 1) pv(j - 1);
+        AT_TR(j * 16 + 3);
+        if (++s == AT_STAGES) { s = 0; ph ^= 1; }
       }
-      if (nt >= 1) pv(nt - 1);
     }
-  } else {  // ---------------- softmax / correction / epilogue ----------------
-    const int q = warp & 3;
+  } else if (warp == AT_WO) {
+    if (lane == 0) {  // ---------------- PV issuer: O += P_j X~_j ----------------
+      constexpr uint32_t idesc_o = idesc_bf16(AT_BM, AT_D, 1);  // B MN-major
+      const uint32_t aX = smem_u32(sX);
+      int s = 0;
+      for (int j = 0; j < nt; ++j) {
+        const int b = j & 1;
+        mbar_wait(&p_full[b], (j >> 1) & 1);
+        AT_TR(j * 16 + 4);
+        tc_fence_after();
+        const uint32_t xs = aX + s * AT_X_BYTES;
+#pragma unroll
+        for (int k = 0; k < AT_BN / 16; ++k)
+          umma_f16_ts(tmem + AT_TO, tmem + AT_TS + b * AT_BN + k * 8,
+                      sdesc_sw128(xs + k * 2048, AT_X_BYTES / 2, 1024), idesc_o, (j | k) != 0);
+        umma_commit(&pv_done[b]);
+        umma_commit(&x_empty[s]);
+        AT_TR(j * 16 + 5);
+        if (++s == AT_STAGES) s = 0;
+      }
+    }
+  } else {  // -------- softmax / correction / epilogue: AT_NSW warps, one row x AT_CW key columns each --------
+    const int q = warp & 3, pp = warp >> 2;  // TMEM lane quarter, key-column part
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float m = -INFINITY, l = 0.f;
+    {  // U row (this thread's AT_CW of d columns) -> TMEM as packed bf16 pairs: the A operand of S
+      const int64_t grow = it.qrow0 + row;
+      const uint4 *src = reinterpret_cast<const uint4 *>(U + grow * AT_D + AT_CW * pp);
+#pragma unroll
+      for (int h16 = 0; h16 < AT_CW / 32; ++h16) {  // 32 bf16 = 16 packed columns per store
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint4 v = grow < NQ ? src[4 * h16 + k] : make_uint4(0, 0, 0, 0);
+          w[4 * k] = v.x;
+          w[4 * k + 1] = v.y;
+          w[4 * k + 2] = v.z;
+          w[4 * k + 3] = v.w;
+        }
+        tmem_st16(tmem + lane_off + AT_TU + (AT_CW / 2) * pp + 16 * h16, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(u_full);
+    }
+    float m = -INFINITY, l = 0.f;  // l: this part's share of the row sum
     for (int j = 0; j < nt; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
+      if (warp == 0 && lane == 0) AT_TR(j * 16 + 6);
       tc_fence_after();
-      const int kvalid = it.klen - j * AT_BN;  // keys of this tile that belong to the chunk
-      uint32_t sr[128];
+      const int kvalid = it.klen - j * AT_BN - AT_CW * pp;  // keys of this part inside the chunk
+      uint32_t sr[AT_CW];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t (&r)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]);
-        tmem_ld32(tS + lane_off + b * AT_BN + 32 * c, r);
-      }
+      for (int c = 0; c < AT_CW; c += 32)
+        tmem_ld32(tmem + lane_off + AT_TS + b * AT_BN + AT_CW * pp + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
       tmem_ld_wait();
-      float mt = -INFINITY;
+      float mx[8];
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        float v = c < kvalid ? __uint_as_float(sr[c]) : -INFINITY;
-        sr[c] = __float_as_uint(v);
-        mt = fmaxf(mt, v);
+      for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+      const bool partial = kvalid < AT_CW;  // warp-uniform: only a chunk's last tile needs the mask
+      if (partial) {
+#pragma unroll
+        for (int c = 0; c < AT_CW; ++c)
+          if (c >= kvalid) sr[c] = __float_as_uint(-INFINITY);
       }
+#pragma unroll
+      for (int c = 0; c < AT_CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], __uint_as_float(sr[c]));
+      sMax[(b * AT_NP + pp) * 128 + row] = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      if (warp == 0 && lane == 0) AT_TR(j * 16 + 7);
+      named_bar_sync(1, 32 * AT_NSW);  // every part's S columns are in registers and its maximum posted
+      if (warp == 0 && lane == 0) AT_TR(j * 16 + 8);
+      float mt = sMax[(b * AT_NP) * 128 + row];
+#pragma unroll
+      for (int k = 1; k < AT_NP; ++k) mt = fmaxf(mt, sMax[(b * AT_NP + k) * 128 + row]);
       const bool need = mt > m + AT_RESCALE_THRESHOLD;
       if (j == 0) {
         m = mt;
       } else if (__any_sync(0xffffffffu, need)) {
-        // warp-uniform (tcgen05.ld/st are .sync.aligned): O = O * 2^(m - m_new) per row once
-        // every PV issued so far has landed; rows that do not need it use scale 1
+        // warp-uniform: this part of O *= 2^(m - m_new) per row once every PV issued so far has landed
         mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
         const float mnew = need ? mt : m;
         const float sc = exp2f(m - mnew);
         l *= sc;
 #pragma unroll 1
-        for (int c = 0; c < AT_D; c += 16) {
+        for (int c = 0; c < AT_CW; c += 16) {
           uint32_t o[16];
-          tmem_ld16(tO + lane_off + c, o);
+          tmem_ld16(tmem + lane_off + AT_TO + AT_CW * pp + c, o);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
-          tmem_st16(tO + lane_off + c, o);
+          tmem_st16(tmem + lane_off + AT_TO + AT_CW * pp + c, o);
         }
         tmem_st_wait();
         m = mnew;
       }
-      // P = 2^(S - m) (bf16), row sum of the rounded values
-      if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // MMA of tile j-2 done reading P buffer b
-      uint8_t *pb = sP + b * AT_P_BYTES;
-      float ls = 0.f;
+      // P = 2^(S - m) as bf16 pairs: keys [AT_CW pp, AT_CW (pp + 1)) -> S buffer b columns
+      // [AT_CW/2 pp, AT_CW/2 (pp + 1)).  Packed fp32x2 arithmetic; on full tiles 3 of every 8 pairs
+      // of exponentials run on the FMA pipe (ex2_fma2): at d = 128 one exp per (row, key) balances
+      // MUFU and the tensor pipe exactly.  The row sum accumulates the fp32 values.
+      const uint64_t nm2 = f2_pack(-m, -m);
+      uint64_t ls2[2] = {0ull, 0ull};
+      uint32_t w[AT_CW / 2];
+      if (partial) {  // masked keys must give exactly 0: MUFU ex2(-inf) = 0
 #pragma unroll
-      for (int c8 = 0; c8 < 16; ++c8) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float p0 = ex2(__uint_as_float(sr[8 * c8 + 2 * i]) - m);
-          const float p1 = ex2(__uint_as_float(sr[8 * c8 + 2 * i + 1]) - m);
-          w[i] = pack_bf16(p0, p1);
-          __nv_bfloat162 h2 = *reinterpret_cast<__nv_bfloat162 *>(&w[i]);
-          ls += __low2float(h2) + __high2float(h2);
+        for (int i = 0; i < AT_CW / 2; ++i) {
+          const uint64_t x2 = f2_add((uint64_t)sr[2 * i] | ((uint64_t)sr[2 * i + 1] << 32), nm2);
+          const uint64_t e2 = f2_pack(ex2(f2_lo(x2)), ex2(f2_hi(x2)));
+          w[i] = pack_bf16(f2_lo(e2), f2_hi(e2));
+          ls2[i & 1] = f2_add(ls2[i & 1], e2);
         }
-        const uint32_t off = (c8 >> 3) * (AT_P_BYTES / 2) + sw128_off(row, c8 & 7);
-        *reinterpret_cast<uint4 *>(pb + off) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < AT_CW / 2; ++i) {
+          const uint64_t x2 = f2_add((uint64_t)sr[2 * i] | ((uint64_t)sr[2 * i + 1] << 32), nm2);
+          uint64_t e2;
+          if ((i & 7) == 1 || (i & 7) == 4 || (i & 7) == 6)
+            e2 = ex2_fma2(f2_pack(fmaxf(f2_lo(x2), -126.f), fmaxf(f2_hi(x2), -126.f)));
+          else
+            e2 = f2_pack(ex2(f2_lo(x2)), ex2(f2_hi(x2)));
+          w[i] = pack_bf16(f2_lo(e2), f2_hi(e2));
+          ls2[i & 1] = f2_add(ls2[i & 1], e2);
+        }
       }
-      l += ls;
-      fence_proxy_async();
+      const uint64_t lsum = f2_add(ls2[0], ls2[1]);
+      if (warp == 0 && lane == 0) AT_TR(j * 16 + 12);
+#pragma unroll
+      for (int c = 0; c < AT_CW / 2; c += 16)
+        tmem_st16(tmem + lane_off + AT_TS + b * AT_BN + (AT_CW / 2) * pp + c, *reinterpret_cast<uint32_t(*)[16]>(&w[c]));
+      l += f2_lo(lsum) + f2_hi(lsum);
+      tmem_st_wait();
+      if (warp == 0 && lane == 0) AT_TR(j * 16 + 13);
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (lane == 0 && (warp == 0 || warp == 4 || warp == AT_NSW - 1))
+        AT_TR(j * 16 + 9 + (warp == 0 ? 0 : warp == 4 ? 1 : 2));
     }
-    // epilogue: wait for the last PV, then write Y = O / l or the (m, l, O) partial
+    // epilogue: wait for the last PV, combine the parts' sums, write this part of Y or of the partial
     if (nt >= 1) mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
     tc_fence_after();
+    sSum[pp * 128 + row] = l;
+    named_bar_sync(1, 32 * AT_NSW);
+    float lrow = 0.f;
+#pragma unroll
+    for (int k = 0; k < AT_NP; ++k) lrow += sSum[k * 128 + row];
     const bool ok = row < it.nq;
-    if (it.part_row < 0) {
-      const float inv = 1.f / l;
-      bf16 *yr = Y + (it.qrow0 + row) * AT_D;
 #pragma unroll 1
-      for (int c = 0; c < AT_D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tO + lane_off + c, o);
-        tmem_ld_wait();
-        if (ok) {
-          uint4 *dst = reinterpret_cast<uint4 *>(yr + c);
+    for (int cb = 0; cb < AT_CW; cb += 32) {
+    uint32_t o[32];
+    tmem_ld32(tmem + lane_off + AT_TO + AT_CW * pp + cb, o);
+    tmem_ld_wait();
+    if (ok) {
+      if (it.part_row < 0) {
+        const float inv = 1.f / lrow;
+        uint4 *dst = reinterpret_cast<uint4 *>(Y + (it.qrow0 + row) * AT_D + AT_CW * pp + cb);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
+      } else {
+        float *pr = part + (it.part_row + row) * (int64_t)(AT_D + 2);
+        if (pp == 0 && cb == 0) {
+          pr[0] = m;
+          pr[1] = lrow;
         }
-      }
-    } else {
-      float *pr = part + (it.part_row + row) * (int64_t)(AT_D + 2);
-      if (ok) {
-        pr[0] = m;
-        pr[1] = l;
-      }
-#pragma unroll 1
-      for (int c = 0; c < AT_D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tO + lane_off + c, o);
-        tmem_ld_wait();
-        if (ok) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            *reinterpret_cast<float2 *>(pr + 2 + c + i) = make_float2(__uint_as_float(o[i]), __uint_as_float(o[i + 1]));
-        }
+        for (int i = 0; i < 32; i += 2)
+          *reinterpret_cast<float2 *>(pr + 2 + AT_CW * pp + cb + i) =
+              make_float2(__uint_as_float(o[i]), __uint_as_float(o[i + 1]));
       }
+    }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tmem, 512);
+  if (warp == AT_WS) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace tc
@@ -260,18 +326,30 @@ cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, 
                          int64_t n_items, int d, void *Y, float *part, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   if (d != tc::AT_D) return cudaErrorInvalidValue;
-  // U is [NQ x d]: query-tile rows past NQ are zero-filled by TMA (and never written back)
-  CUtensorMap mu, mx;
-  if (!tc::make_map_bf16(&mu, U, NQ, d, d, 128) || !tc::make_map_bf16(&mx, Xt, T2, d, d, 128))
-    return cudaErrorInvalidValue;
+  CUtensorMap mx;
+  if (!tc::make_map_bf16(&mx, Xt, T2, d, d, 128)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc::k_tc_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::AT_SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  unsigned long long *trace = nullptr;
+  const char *trace_path = getenv("STCA_TRACE_ATTN");  // debug only: clock64 stamps of work item 0
+  if (trace_path && cudaMalloc(&trace, 8192 * 8) == cudaSuccess) cudaMemsetAsync(trace, 0, 8192 * 8, st);
   note_launch();
-  tc::k_tc_attention<<<(unsigned)n_items, 192, tc::AT_SMEM, st>>>(mu, mx, items, (bf16 *)Y, part);
+  tc::k_tc_attention<<<(unsigned)n_items, tc::AT_THREADS, tc::AT_SMEM, st>>>(mx, (const bf16 *)U, NQ, items,
+                                                                               (bf16 *)Y, part, trace);
+  if (trace) {
+    static unsigned long long h[8192];
+    cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(trace);
+    if (FILE *f = fopen(trace_path, "wb")) {
+      fwrite(h, sizeof h, 1, f);
+      fclose(f);
+    }
+  }
   return cudaGetLastError();
 }
 

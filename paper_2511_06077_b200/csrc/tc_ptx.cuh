@@ -224,6 +224,46 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (ftz)
   return y;
 }
 
+// 2^x on the FMA/ALU pipes (no MUFU): x = j + f with j = rint(x) (1.5*2^23 rounding trick),
+// 2^f on [-1/2, 1/2] by a cubic fit (max relative error 1.0e-4, far below the bf16 rounding
+// of P it feeds), 2^j added to the exponent field.  Valid for x in [-126, 0].
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  const float p = fmaf(fmaf(fmaf(0.05500802f, f, 0.24220887f), f, 0.69328306f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// packed fp32x2 arithmetic (sm_100a FADD2 / FFMA2): two lanes of work per issued instruction
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// 2^x for two lanes on the FMA/ALU pipes (ex2_fma below, packed); x already clamped to >= -126
+__device__ __forceinline__ uint64_t ex2_fma2(uint64_t x) {
+  const uint64_t mag = f2_pack(12582912.f, 12582912.f), nmag = f2_pack(-12582912.f, -12582912.f);
+  const uint64_t t = f2_add(x, mag);
+  const uint64_t f = f2_add(x, f2_add(t, nmag) ^ 0x8000000080000000ull);  // x - rint(x)
+  uint64_t p = f2_fma(f2_pack(0.05500802f, 0.05500802f), f, f2_pack(0.24220887f, 0.24220887f));
+  p = f2_fma(p, f, f2_pack(0.69328306f, 0.69328306f));
+  p = f2_fma(p, f, f2_pack(1.0f, 1.0f));
+  const uint32_t lo = (uint32_t)p + ((uint32_t)t << 23), hi = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low 16 bits), .y = b
   return *reinterpret_cast<uint32_t *>(&v);
