@@ -147,3 +147,13 @@ def test_full_size_sampled(name):
     sample = sorted({0, int(np.argmin(L)), int(np.argmax(L))})
     check(wl, Z, z, TOL["bf16"], requests=sample)
     assert np.isfinite(Z).all() and np.isfinite(z).all()
+
+
+def test_capacity_shape_d512_sampled():
+    """BASELINE capacity config shape (d = 512, h = 8, M = 8, 32 targets per request), a few ragged
+    requests up to L = 10k: the 2-GEMM tcgen05 projection (LayerNorm over a 512-wide TMEM row) and
+    the CUDA-core attention sweep."""
+    cfg = workload.CONFIGS["capacity"]
+    wl = workload.make_workload(cfg, seed=2, B=4, lengths=np.array([10000, 64, 1500, 4104]))
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["bf16"])
