@@ -722,7 +722,8 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
   const bool tc_attn = h->bf16 && stca::tc_available() && stca::tc_attention_supported(d);
-  const int qtile = tc_attn ? 128 : 16;
+  const bool tc_wide = h->bf16 && stca::tc_available() && stca::tc_attention_wide_supported(d);
+  const int qtile = tc_attn ? 128 : tc_wide ? 64 : 16;
   std::vector<int64_t> it6;
   int64_t nit = stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, nullptr, 0);
   it6.resize((size_t)std::max<int64_t>(nit, 1) * 6);
@@ -787,6 +788,9 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     if (tc_attn) {
       CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+    } else if (tc_wide) {
+      CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
+                                 h->part.as<float>(), st));
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     }
