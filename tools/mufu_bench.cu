@@ -20,6 +20,12 @@ __global__ void k(int iters, float *out, unsigned long long *cyc) {
       if (OP == 1) asm volatile("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(a[i]));
       if (OP == 2) asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a[i]));
       if (OP == 3) y = stca::tc::ex2_fma(a[i]);
+      if (OP == 4 || OP == 5) {  // packed half-precision tanh: two results per op (counted as 2)
+        uint32_t x = __float_as_uint(a[i]), r;
+        if (OP == 4) asm volatile("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+        else asm volatile("tanh.approx.bf16x2 %0, %1;" : "=r"(r) : "r"(x));
+        y = __uint_as_float(r ^ 0x80008000u);
+      }
       a[i] = y * -0.999f;
     }
   }
@@ -42,7 +48,7 @@ void run(const char *name) {
   k<OP><<<1, threads>>>(iters, o, c);
   cudaDeviceSynchronize();
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-  printf("%-22s %6.2f ops/clk/SM\n", name, (double)iters * 8 * threads / h);
+  printf("%-22s %6.2f results/clk/SM\n", name, (double)iters * 8 * threads / h * (OP >= 4 ? 2 : 1));
 }
 
 int main() {
@@ -50,5 +56,7 @@ int main() {
   run<1>("tanh.approx.f32");
   run<2>("rcp.approx.ftz.f32");
   run<3>("ex2_fma (FMA pipe)");
+  run<4>("tanh.approx.f16x2");
+  run<5>("tanh.approx.bf16x2");
   return 0;
 }
