@@ -98,10 +98,15 @@ stca_status stca_create(const stca_config *cfg, const stca_tensor *weights, int3
  *   X~(i) = LN(SwiGLUFFN(i)(X_b[start'_b:end_b]))  for every layer i and request b,
  * start'_b = max(hist_off[b], hist_off[b+1] - L_infer).  X is [T x d] row-major,
  * bf16 (uint16 bit patterns) or fp32 per cfg.dtype, rows chronological (oldest
- * first), device OR host memory (host buffers are staged H2D on `stream`).
- * hist_off is a HOST int64 array [B+1], consumed before return.  The handle
- * owns the projected cache until the next call or destroy.  On any error
- * nothing is enqueued. */
+ * first), device OR host memory.  A host X (pinned for asynchrony) is streamed
+ * up in pieces on a handle-owned copy stream that waits only for the previous
+ * call's reads of the staging buffer, and each piece is projected on `stream`
+ * as soon as it has landed (the upload overlaps the projection and any earlier
+ * work on `stream`); with L_infer truncation it is staged whole on `stream`.
+ * A host X must stay valid and unmodified until `stream` has completed this
+ * call's work.  hist_off is a HOST int64 array [B+1], consumed before return.
+ * The handle owns the projected cache until the next call or destroy.  On a
+ * validation error nothing is enqueued. */
 stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
                                  int64_t B, void *stream);
 
@@ -109,7 +114,10 @@ stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const
  * xt [Nt x d] (dtype per cfg, device or host), tgt_off HOST int64 [B+1]
  * (request b owns target rows [tgt_off[b], tgt_off[b+1]); m_b = 0 is legal).
  * Outputs (device or host, float32): out_Z [Nt x M x d] = Z_H rows (Eq.(8)),
- * out_z [Nt x d] or NULL.  Any number of forwards may reuse one projection. */
+ * out_z [Nt x d] or NULL.  Everything is enqueued on `stream` and the call does
+ * not wait: host inputs must stay valid and host outputs are complete only once
+ * `stream` has completed this call's work (use pinned memory for asynchrony).
+ * Any number of forwards may reuse one projection. */
 stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                          float *out_Z, float *out_z, void *stream);
 

@@ -53,6 +53,21 @@ def _stream(stream) -> int:
     return 0
 
 
+def _is_cuda(x) -> bool:
+    return bool(getattr(x, "is_cuda", False))
+
+
+def _synchronize(stream) -> None:
+    """Wait for `stream` (torch stream, raw cudaStream_t int, or None = torch's current stream)."""
+    import torch
+    if stream is None:
+        torch.cuda.current_stream().synchronize()
+    elif isinstance(stream, int):
+        torch.cuda.ExternalStream(stream).synchronize()
+    else:
+        stream.synchronize()
+
+
 def _i64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
 
@@ -127,8 +142,12 @@ class STCA:
                                                 ctypes.c_void_p(_stream(stream))))
         self._B = B
 
-    def forward(self, xt, tgt_off, out_Z, out_z=None, stream=None) -> None:
-        """Eq.(3)-(9) for the targets of the projected requests; writes out_Z [Nt,M,d], out_z [Nt,d]."""
+    def forward(self, xt, tgt_off, out_Z, out_z=None, stream=None, sync=None) -> None:
+        """Eq.(3)-(9) for the targets of the projected requests; writes out_Z [Nt,M,d], out_z [Nt,d].
+
+        The C call only enqueues work on `stream`.  With host (numpy) outputs the binding waits for the
+        stream before returning unless sync=False (then the caller synchronises, e.g. with pinned torch
+        CPU tensors in a pipelined serving loop)."""
         off = _i64(tgt_off)
         B = off.shape[0] - 1
         Nt = int(xt.shape[0])
@@ -136,6 +155,9 @@ class STCA:
                                        off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
                                        ctypes.c_void_p(_ptr(out_Z)), ctypes.c_void_p(_ptr(out_z)),
                                        ctypes.c_void_p(_stream(stream))))
+        host_out = any(o is not None and not _is_cuda(o) for o in (out_Z, out_z))
+        if sync or (sync is None and host_out):
+            _synchronize(stream)
 
 
 # ---------------------------------------------------------------------------

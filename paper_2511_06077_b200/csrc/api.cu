@@ -15,6 +15,8 @@
 #include "launch.h"
 #include "tc.h"
 
+#define STCA_H2D_PIECES 8  // pieces of a pipelined host-input projection
+
 using stca::bf16;
 
 #include <atomic>
@@ -101,6 +103,9 @@ struct stca_handle {
   DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, zout, Zout;
   HostPinned pin;
   int64_t chunk_cap = 4096;
+  // pipelined host-input projection: copy stream + one event per piece
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_xin_free = nullptr, ev[STCA_H2D_PIECES] = {};
 };
 
 static thread_local std::string g_create_error;  // message of the last failed stca_create on this thread
@@ -516,6 +521,11 @@ extern "C" void stca_destroy(stca_handle *h) {
                     &h->part,     &h->partg, &h->items, &h->mitems, &h->zout,  &h->Zout};
   for (DevBuf *b : bufs) b->release();
   h->pin.release();
+  if (h->copy_st) {
+    cudaStreamDestroy(h->copy_st);
+    cudaEventDestroy(h->ev_xin_free);
+    for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  }
   cudaGetLastError();
   delete h;
 }
@@ -525,6 +535,54 @@ extern "C" const char *stca_last_error(const stca_handle *h) { return h ? h->err
 // ===========================================================================
 // project_history
 // ===========================================================================
+// a1: X~(i) = LN(SwiGLUFFN(i)(X)) for all layers, Eq.(2), for cache rows [r0, r0 + rows) (X points at
+// row r0 of the compacted input)
+static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64_t rows, cudaStream_t st) {
+  const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
+  const size_t row_bytes = (size_t)d * es;
+  const int64_t T2 = h->T2;
+  if (h->bf16 && stca::tc_available()) {
+    stca::TcProj pj;
+    pj.X = X;
+    pj.rows = rows;
+    pj.d = d;
+    pj.rd = rd;
+    pj.M = M;
+    pj.eps = h->cfg.ln_eps;
+    pj.out = (uint8_t *)h->xt_cache.p + (size_t)r0 * row_bytes;
+    pj.out_layer_stride = T2 * d;
+    pj.W1cat = h->tcp.W1cat;
+    pj.Wocat = h->tcp.Wocat;
+    pj.gcat = h->tcp.gcat;
+    pj.bcat = h->tcp.bcat;
+    for (int i = 0; i < M; ++i) {
+      pj.W1[i] = h->L[i].tc.W1h;
+      pj.Wo[i] = h->L[i].tc.Woh;
+      pj.g[i] = h->L[i].gh;
+      pj.b[i] = h->L[i].bh;
+    }
+    CU(stca::tc_project(pj, st));
+    return STCA_OK;
+  }
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
+  CU(h->proj_h.ensure((size_t)R * rd * es));
+  CU(h->proj_y.ensure((size_t)R * d * 4));
+  for (int i = 0; i < M; ++i) {
+    for (int64_t q0 = 0; q0 < rows; q0 += R) {
+      const int n = (int)std::min<int64_t>(R, rows - q0);
+      const uint8_t *xa = (const uint8_t *)X + (size_t)q0 * row_bytes;
+      CU(stca::cc_gemm(h->bf16, xa, d, h->L[i].W1h, 2 * rd, h->proj_h.p, rd, nullptr, 0, n, 2 * rd, d, 1.f,
+                       stca::EPI_SWIGLU, st));
+      CU(stca::cc_gemm(h->bf16, h->proj_h.p, rd, h->L[i].Woh, d, nullptr, 0, h->proj_y.as<float>(), d, n, d, rd,
+                       1.f, stca::EPI_STORE, st));
+      uint8_t *dst = (uint8_t *)h->xt_cache.p + ((size_t)i * T2 + r0 + q0) * row_bytes;
+      CU(stca::cc_layernorm(h->bf16, h->proj_y.as<float>(), d, h->L[i].gh, h->L[i].bh, h->cfg.ln_eps, dst, d, n, d,
+                            st));
+    }
+  }
+  return STCA_OK;
+}
+
 extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
                                             int64_t B, void *stream) {
   if (!h) return STCA_ERR_INVALID_ARG;
@@ -566,8 +624,40 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     gather |= h->start[b] + h->own0[b] != hist_off[b] || h->olen[b] != hist_off[b + 1] - hist_off[b];
   }
   const int64_t T2 = h->coff[B];  // rows of the X~ cache (the suffix rows this rank owns)
+  CU(h->xt_cache.ensure((size_t)M * T2 * row_bytes + 256));
+  h->T2 = T2;
   const void *Xd = X;
-  if (T > 0 && !is_device_ptr(X)) {  // host input: stage H2D on the stream
+  const bool host_x = T > 0 && !is_device_ptr(X);
+  if (host_x && !gather && T2 > 0) {
+    // host input, no gather: stream X up in pieces on a copy stream and project each piece as soon as
+    // it has landed, so the H2D copy (the e2e bottleneck) overlaps the projection of earlier pieces
+    CU(h->xin.ensure((size_t)T * row_bytes));
+    if (!h->copy_st) {
+      CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&h->ev_xin_free, cudaEventDisableTiming));
+      for (cudaEvent_t &e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // the copies only wait for the previous projection's reads of xin (ev_xin_free), not for other
+    // work on `stream`: the next request batch's upload overlaps the current forward
+    CU(cudaStreamWaitEvent(h->copy_st, h->ev_xin_free, 0));
+    const int npieces = (int)std::min<int64_t>(STCA_H2D_PIECES, (T2 + (1 << 16) - 1) >> 16);
+    const int64_t step = ((T2 + npieces - 1) / npieces + 255) / 256 * 256;  // whole 128-row tile pairs
+    int k = 0;
+    for (int64_t r0 = 0; r0 < T2; r0 += step, ++k) {
+      const int64_t rows = std::min<int64_t>(step, T2 - r0);
+      uint8_t *dst = (uint8_t *)h->xin.p + (size_t)r0 * row_bytes;
+      CU(cudaMemcpyAsync(dst, (const uint8_t *)X + (size_t)r0 * row_bytes, (size_t)rows * row_bytes,
+                         cudaMemcpyHostToDevice, h->copy_st));
+      CU(cudaEventRecord(h->ev[k], h->copy_st));
+      CU(cudaStreamWaitEvent(st, h->ev[k], 0));
+      stca_status s = project_rows(h, dst, r0, rows, st);
+      if (s != STCA_OK) return s;
+    }
+    CU(cudaEventRecord(h->ev_xin_free, st));
+    h->B = B;
+    return STCA_OK;
+  }
+  if (host_x) {  // host input with a gather: stage all of X on the stream first
     CU(h->xin.ensure((size_t)T * row_bytes));
     CU(cudaMemcpyAsync(h->xin.p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
     Xd = h->xin.p;
@@ -590,48 +680,11 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), B, maxlen, (int)row_bytes, st));
     Xd = h->xgather.p;
   }
-  CU(h->xt_cache.ensure((size_t)M * T2 * row_bytes + 256));
-  h->T2 = T2;
-  // a1: X~(i) = LN(SwiGLUFFN(i)(X)) for all layers, Eq.(2)
-  if (h->bf16 && stca::tc_available()) {
-    stca::TcProj pj;
-    pj.X = Xd;
-    pj.rows = T2;
-    pj.d = d;
-    pj.rd = rd;
-    pj.M = M;
-    pj.eps = h->cfg.ln_eps;
-    pj.out = h->xt_cache.p;
-    pj.out_layer_stride = T2 * d;
-    pj.W1cat = h->tcp.W1cat;
-    pj.Wocat = h->tcp.Wocat;
-    pj.gcat = h->tcp.gcat;
-    pj.bcat = h->tcp.bcat;
-    for (int i = 0; i < M; ++i) {
-      pj.W1[i] = h->L[i].tc.W1h;
-      pj.Wo[i] = h->L[i].tc.Woh;
-      pj.g[i] = h->L[i].gh;
-      pj.b[i] = h->L[i].bh;
-    }
-    CU(stca::tc_project(pj, st));
-  } else {
-    const int64_t R = std::min<int64_t>(std::max<int64_t>(T2, 1), 1 << 16);
-    CU(h->proj_h.ensure((size_t)R * rd * es));
-    CU(h->proj_y.ensure((size_t)R * d * 4));
-    for (int i = 0; i < M; ++i) {
-      for (int64_t r0 = 0; r0 < T2; r0 += R) {
-        const int rows = (int)std::min<int64_t>(R, T2 - r0);
-        const uint8_t *xa = (const uint8_t *)Xd + (size_t)r0 * row_bytes;
-        CU(stca::cc_gemm(h->bf16, xa, d, h->L[i].W1h, 2 * rd, h->proj_h.p, rd, nullptr, 0, rows, 2 * rd, d, 1.f,
-                         stca::EPI_SWIGLU, st));
-        CU(stca::cc_gemm(h->bf16, h->proj_h.p, rd, h->L[i].Woh, d, nullptr, 0, h->proj_y.as<float>(), d, rows, d, rd,
-                         1.f, stca::EPI_STORE, st));
-        uint8_t *dst = (uint8_t *)h->xt_cache.p + ((size_t)i * T2 + r0) * row_bytes;
-        CU(stca::cc_layernorm(h->bf16, h->proj_y.as<float>(), d, h->L[i].gh, h->L[i].bh, h->cfg.ln_eps, dst, d, rows,
-                              d, st));
-      }
-    }
+  if (T2 > 0) {
+    stca_status s = project_rows(h, Xd, 0, T2, st);
+    if (s != STCA_OK) return s;
   }
+  if (host_x && h->ev_xin_free) CU(cudaEventRecord(h->ev_xin_free, st));
   h->B = B;
   return STCA_OK;
 }
@@ -824,7 +877,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   }
   if (Z_host) CU(cudaMemcpyAsync(out_Z, Zd, (size_t)Nt * M * d * 4, cudaMemcpyDeviceToHost, st));
   if (z_host) CU(cudaMemcpyAsync(out_z, zd, (size_t)Nt * d * 4, cudaMemcpyDeviceToHost, st));
-  if (Z_host || z_host) CU(cudaStreamSynchronize(st));
+  // host outputs: asynchronous like every other result (complete once `stream` reaches this point)
   CU(cudaGetLastError());
   return STCA_OK;
 }

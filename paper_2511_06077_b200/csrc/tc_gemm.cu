@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // bf16 [n2 x n1 x n0] (n0 innermost, contiguous), box = box1 rows x 64 x 1, SWIZZLE_128B
-bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1);
+bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1, int64_t s2 = 0);
 
 // ---------------------------------------------------------------------------
 // host side
@@ -262,11 +262,12 @@ bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, 
   return r == CUDA_SUCCESS;
 }
 
-bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1) {
+// bf16 [n2 x n1 x n0] (n0 contiguous; dim-2 stride s2 elements, default n1 * n0); box = 64 x box1 x 1
+bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1, int64_t s2) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t gdim[3] = {(cuuint64_t)n0, (cuuint64_t)n1, (cuuint64_t)n2};
-  cuuint64_t gstride[2] = {(cuuint64_t)(n0 * 2), (cuuint64_t)(n1 * n0 * 2)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(n0 * 2), (cuuint64_t)((s2 ? s2 : n1 * n0) * 2)};
   cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
   cuuint32_t estride[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), gdim, gstride, box, estride,

@@ -39,7 +39,7 @@ namespace stca {
 namespace tc {
 
 bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
-bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1);
+bool make_map_bf16_3d(CUtensorMap *m, const void *ptr, int64_t n2, int64_t n1, int64_t n0, int box1, int64_t s2);
 
 constexpr int PJ_D = 128;                            // d (row width of X and X~)
 constexpr int PJ_ROWS = 128;                         // rows per CTA
@@ -502,11 +502,11 @@ cudaError_t tc_project(const TcProj &p, cudaStream_t st) {
   if (p.rows <= 0) return cudaSuccess;
   if (p.d == tc::PJ_D && p.rd % (2 * tc::PJ_NCH) == 0 && p.rd >= 4 * tc::PJ_NCH &&  // an even number >= 4 of chunks per layer
       p.W1cat && p.Wocat && p.gcat && p.bcat &&
-      p.out_layer_stride == p.rows * p.d && p.M <= tc::PJ_MAXM) {
+      p.out_layer_stride >= p.rows * p.d && p.out_layer_stride % 8 == 0 && p.M <= tc::PJ_MAXM) {
     CUtensorMap m1, mo, mout, mx;
     if (!tc::make_map_bf16(&m1, p.W1cat, (int64_t)p.M * 2 * p.rd, p.d, p.d, 2 * tc::PJ_NCH) ||
         !tc::make_map_bf16(&mo, p.Wocat, (int64_t)p.M * p.rd, p.d, p.d, tc::PJ_NCH) ||
-        !tc::make_map_bf16_3d(&mout, p.out, p.M, p.rows, p.d, tc::PJ_ROWS) ||
+        !tc::make_map_bf16_3d(&mout, p.out, p.M, p.rows, p.d, tc::PJ_ROWS, p.out_layer_stride) ||
         !tc::make_map_bf16(&mx, p.X, p.rows, p.d, p.d, tc::PJ_ROWS))
       return cudaErrorInvalidValue;
     auto kern = tc::k_tc_project;

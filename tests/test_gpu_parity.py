@@ -96,6 +96,17 @@ def test_host_buffers_equal_device_buffers():
     assert np.array_equal(Zd, Zh) and np.array_equal(zd, zh)
 
 
+def test_host_input_pipelined_bit_exact():
+    """Host X large enough to be streamed up in several pieces (copy stream overlapping the projection,
+    include/stca.h): outputs bit-identical to device-resident inputs; the suffix-gather variant too."""
+    for L_infer in (0, 7000):
+        cfg = make_cfg(B=24, m=8, L_infer=L_infer)
+        wl = workload.make_workload(cfg, seed=9, lengths=np.array([10000, 9999, 1, 8191] * 6))
+        Zd, zd = run_gpu(wl)
+        Zh, zh = run_gpu(wl, host=True)
+        assert np.array_equal(Zd, Zh) and np.array_equal(zd, zh), L_infer
+
+
 def test_single_key_history_exact_weight():
     """P4: L_b = 1 -> alpha = 1: the attention output is the (bf16) X~ row itself, so o is
     independent of the query; two different targets give identical Z."""
