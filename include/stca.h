@@ -157,6 +157,11 @@ void stca_plan_split(int64_t L, int32_t chunk_keys, int32_t G, int32_t g, int64_
  * part_out[b] in [0, n_parts). */
 void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *part_out);
 
+/* Persistent-kernel schedule: n work items of `cost` over n_ctas CTAs by the LPT rule of
+ * stca_plan_shards (bin_out[i] = CTA of item i), written as CSR into cta_list:
+ * [n_ctas + 1] offsets, then the item indices of each CTA in descending cost (ties by index). */
+void stca_plan_persistent(const int64_t *cost, int64_t n, int32_t n_ctas, int32_t *cta_list, int32_t *bin_out);
+
 #ifdef __cplusplus
 }
 #endif

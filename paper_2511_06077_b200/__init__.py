@@ -18,11 +18,11 @@ from typing import Dict, Optional
 
 import numpy as np
 
-from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_shards,  # noqa: F401
+from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_persistent, plan_shards,  # noqa: F401,E501
                    plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, _Config,
                    _Tensor, LIB_PATH)
 
-__all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_shards", "plan_split", "plan_suffix",
+__all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_persistent", "plan_shards", "plan_split", "plan_suffix",
            "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange"]
 
 

@@ -38,7 +38,7 @@ _I64P = ctypes.POINTER(ctypes.c_int64)
 SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy", "stca_last_error",
            "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
-           "stca_plan_split"]
+           "stca_plan_split", "stca_plan_persistent"]
 
 
 def lib():
@@ -79,6 +79,9 @@ def lib():
         L.stca_plan_shards.restype = None
         L.stca_plan_split.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I64P, _I64P]
         L.stca_plan_split.restype = None
+        L.stca_plan_persistent.argtypes = [_I64P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                           ctypes.POINTER(ctypes.c_int32)]
+        L.stca_plan_persistent.restype = None
         _lib = L
     return _lib
 
@@ -125,6 +128,17 @@ def plan_attention(hist_len, tgt_off, h: int, qtile: int, chunk_keys: int = 0) -
     out = np.zeros((max(n, 1), 6), dtype=np.int64)
     lib().stca_plan_attention(_p64(hl), _p64(t), B, h, qtile, chunk_keys, _p64(out), n)
     return out[:n]
+
+
+def plan_persistent(cost, n_ctas: int):
+    """(cta_off [n_ctas + 1], cta_items [n], bin [n]) of the persistent attention schedule."""
+    c = _i64(cost)
+    n = c.shape[0]
+    lst = np.zeros(n_ctas + 1 + n, dtype=np.int32)
+    b = np.zeros(n, dtype=np.int32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    lib().stca_plan_persistent(_p64(c), n, n_ctas, lst.ctypes.data_as(i32p), b.ctypes.data_as(i32p))
+    return lst[:n_ctas + 1], lst[n_ctas + 1:], b
 
 
 def plan_shards(cost, n_parts: int) -> np.ndarray:

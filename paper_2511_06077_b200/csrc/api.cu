@@ -100,7 +100,7 @@ struct stca_handle {
   DevBuf xt_cache;  // M x [T2 x d] storage
   DevBuf xin, xgather, seg, proj_h, proj_y;
   // forward scratch
-  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, zout, Zout;
+  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, ctal, zout, Zout;
   HostPinned pin;
   int64_t chunk_cap = 4096;
   // pipelined host-input projection: copy stream + one event per piece
@@ -273,7 +273,30 @@ void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *
   }
 }
 
+void stca_plan_persistent(const int64_t *cost, int64_t n, int32_t n_ctas, int32_t *cta_list, int32_t *bin_out) {
+  if (n_ctas < 1) n_ctas = 1;
+  stca_plan_shards(cost, n, n_ctas, bin_out);
+  // CSR: cta_list[0 .. n_ctas] offsets, then the items of each CTA in descending cost (stable)
+  std::vector<int64_t> idx((size_t)n);
+  for (int64_t i = 0; i < n; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+    if (bin_out[a] != bin_out[b]) return bin_out[a] < bin_out[b];
+    if (cost[a] != cost[b]) return cost[a] > cost[b];
+    return a < b;
+  });
+  int32_t *off = cta_list, *lst = cta_list + n_ctas + 1;
+  for (int32_t c = 0; c <= n_ctas; ++c) off[c] = 0;
+  for (int64_t i = 0; i < n; ++i) ++off[bin_out[i] + 1];
+  for (int32_t c = 0; c < n_ctas; ++c) off[c + 1] += off[c];
+  for (int64_t i = 0; i < n; ++i) lst[i] = (int32_t)idx[i];
+}
+
 }  // extern "C"
+
+static int32_t *ctal_resize(std::vector<int32_t> &v, int n_ctas, int64_t n) {
+  v.assign((size_t)n_ctas + 1 + (size_t)n, 0);
+  return v.data();
+}
 
 // ===========================================================================
 // create / destroy
@@ -518,7 +541,7 @@ extern "C" void stca_destroy(stca_handle *h) {
   for (void *p : h->allocs) cudaFree(p);
   DevBuf *bufs[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,   &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,  &h->ybuf32, &h->U,      &h->Y,
-                    &h->part,     &h->partg, &h->items, &h->mitems, &h->zout,  &h->Zout};
+                    &h->part,     &h->partg, &h->items, &h->mitems, &h->ctal, &h->zout,  &h->Zout};
   for (DevBuf *b : bufs) b->release();
   h->pin.release();
   if (h->copy_st) {
@@ -814,17 +837,33 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     a.pad = 0;
     a.part_row = part_base[b] < 0 ? -1 : part_base[b] + o[5] * (tgt_off[b + 1] - tgt_off[b]) * hh + (o[1] - tgt_off[b] * hh);
   }
+  nit = (int64_t)items.size();
+  // persistent d = 128 attention: LPT bins of work items over the SMs (cost = key tiles + 2 for the
+  // item's prologue / epilogue), CTA c runs cta_items[cta_off[c] .. cta_off[c+1]) in LPT order
+  int n_ctas = 0;
+  std::vector<int32_t> ctal;  // cta_off [n_ctas + 1] | cta_items [nit]
+  if (tc_attn && nit > 0) {
+    n_ctas = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit);
+    std::vector<int64_t> cost((size_t)nit);
+    for (int64_t i = 0; i < nit; ++i) cost[i] = (items[i].klen + 127) / 128 + 2;
+    std::vector<int32_t> bin((size_t)nit);
+    stca_plan_persistent(cost.data(), nit, n_ctas, ctal_resize(ctal, n_ctas, nit), bin.data());
+  }
   const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
+  const size_t ctal_bytes = ctal.size() * sizeof(int32_t);
   CU(h->items.ensure(items_bytes + 64));
   CU(h->mitems.ensure(mi_bytes + 64));
-  CU(h->pin.ensure(items_bytes + mi_bytes + 64));
+  CU(h->ctal.ensure(ctal_bytes + 64));
+  CU(h->pin.ensure(items_bytes + mi_bytes + ctal_bytes + 64));
   CU(cudaStreamSynchronize(st));  // the pinned staging buffer may still feed an earlier copy
   memcpy(h->pin.p, items.data(), items_bytes);
   memcpy((uint8_t *)h->pin.p + items_bytes, mi.data(), mi_bytes);
+  memcpy((uint8_t *)h->pin.p + items_bytes + mi_bytes, ctal.data(), ctal_bytes);
   if (items_bytes) CU(cudaMemcpyAsync(h->items.p, h->pin.p, items_bytes, cudaMemcpyHostToDevice, st));
   if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, (uint8_t *)h->pin.p + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
-  nit = (int64_t)items.size();
-  const size_t part_bytes = (size_t)part_rows * (d + 2) * 4;
+  if (ctal_bytes)
+    CU(cudaMemcpyAsync(h->ctal.p, (uint8_t *)h->pin.p + items_bytes + mi_bytes, ctal_bytes, cudaMemcpyHostToDevice, st));
+  const size_t part_bytes = (size_t)part_rows * stca::part_stride(d) * 4;
   if (part_rows) CU(h->part.ensure(part_bytes));
   if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G));
 
@@ -840,7 +879,8 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     if (tc_attn) {
-      CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+      CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
+                            h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
     } else if (tc_wide) {
       CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
                                  h->part.as<float>(), st));

@@ -37,6 +37,9 @@ struct AttnItem {
   int32_t pad;
 };
 
+// Split-K partial row layout (fp32): O[0, d) | m (log2 domain) | l | 2 pad -> 16-byte rows
+__host__ __device__ constexpr int part_stride(int d) { return d + 4; }
+
 // Merge item: one multi-chunk request.
 struct MergeItem {
   int64_t qrow0;     // first query row of the request

@@ -196,14 +196,14 @@ __global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, c
         if (e < d) Y[(it.qrow0 + q) * d + e] = from_f<S>(O[rr][k] * inv);
       }
     } else {
-      float *pr = part + (it.part_row + q) * (int64_t)(d + 2);
+      float *pr = part + (it.part_row + q) * (int64_t)part_stride(d);
       if (lane == 0) {
-        pr[0] = mrow[rr];
-        pr[1] = lrow[rr];
+        pr[d] = mrow[rr];
+        pr[d + 1] = lrow[rr];
       }
       for (int k = 0; k < nd; ++k) {
         int e = lane + 32 * k;
-        if (e < d) pr[2 + e] = O[rr][k];
+        if (e < d) pr[e] = O[rr][k];
       }
     }
   }
@@ -241,26 +241,29 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
   const MergeItem it = items[blockIdx.x];
   const int q = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (q >= it.rows) return;
-  const int64_t stride = (int64_t)it.rows * (d + 2);
-  const float *p0 = part + (it.part_row + q) * (int64_t)(d + 2);
+  const int64_t stride = (int64_t)it.rows * part_stride(d);
+  const float *p0 = part + (it.part_row + q) * (int64_t)part_stride(d);
   // chunk c's partial lives in rank floor(c G / C)'s buffer; offsets computed once per row
   int64_t off[MAXC];
   float w[MAXC];
+  float2 ml[MAXC];  // (m, l) of every chunk: one 8-byte load each, all issued before any use
   float mu = -INFINITY;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (c < it.nchunks) {
       off[c] = (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride;
-      w[c] = __ldg(p0 + off[c]);
-      mu = fmaxf(mu, w[c]);
+      ml[c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d));
     }
   }
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+    if (c < it.nchunks) mu = fmaxf(mu, ml[c].x);
   float l = 0.f;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (c < it.nchunks) {
-      w[c] = exp2f(w[c] - mu);  // fold weight of chunk c (in chunk order below)
-      l += w[c] * __ldg(p0 + off[c] + 1);
+      w[c] = exp2f(ml[c].x - mu);  // fold weight of chunk c (in chunk order below)
+      l += w[c] * ml[c].y;
     }
   }
   const float inv = 1.f / l;
@@ -269,19 +272,22 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c < it.nchunks) {
-        const float2 a0 = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + 2 + e));
-        const float2 a1 = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + 4 + e));
-        acc.x += w[c] * a0.x;
-        acc.y += w[c] * a0.y;
-        acc.z += w[c] * a1.x;
-        acc.w += w[c] * a1.y;
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e));  // 16-byte rows
+        acc.x += w[c] * a.x;
+        acc.y += w[c] * a.y;
+        acc.z += w[c] * a.z;
+        acc.w += w[c] * a.w;
       }
     }
     S *yr = Y + (it.qrow0 + q) * d + e;
-    yr[0] = from_f<S>(acc.x * inv);
-    yr[1] = from_f<S>(acc.y * inv);
-    yr[2] = from_f<S>(acc.z * inv);
-    yr[3] = from_f<S>(acc.w * inv);
+    if constexpr (sizeof(S) == 2) {  // four bf16 in one 8-byte store
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      *reinterpret_cast<uint2 *>(yr) = make_uint2(*reinterpret_cast<const uint32_t *>(&lo),
+                                                  *reinterpret_cast<const uint32_t *>(&hi));
+    } else {
+      *reinterpret_cast<float4 *>(yr) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    }
   }
 }
 

@@ -62,7 +62,10 @@ cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N
 bool tc_attention_wide_supported(int d);
 cudaError_t tc_attention_wide(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                               int64_t n_items, int d, void *Y, float *part, cudaStream_t st);
-cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items, int64_t n_items, int d,
-                         void *Y, float *part, cudaStream_t st);
+// d = 128, persistent: CTA c processes items[cta_items[cta_off[c] .. cta_off[c+1])] in order
+int tc_attention_ctas();  // CTAs of the persistent attention grid (= SM count)
+cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
+                         const int32_t *cta_off, const int32_t *cta_items, int n_ctas, int d, void *Y, float *part,
+                         cudaStream_t st);
 
 }  // namespace stca

@@ -252,14 +252,14 @@ __global__ void __launch_bounds__(352, 1)
                                 pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
                                 pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
         } else {
-          float *pr = part + (it.part_row + r) * (int64_t)(D + 2);
+          float *pr = part + (it.part_row + r) * (int64_t)part_stride(D);
           if (col == 0) {
-            pr[0] = sMax[r] > sMax[64 + r] ? sMax[r] : sMax[64 + r];
-            pr[1] = l;
+            pr[D] = sMax[r] > sMax[64 + r] ? sMax[r] : sMax[64 + r];
+            pr[D + 1] = l;
           }
 #pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            *reinterpret_cast<float2 *>(pr + 2 + col + i) = make_float2(__uint_as_float(o[i]), __uint_as_float(o[i + 1]));
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<uint4 *>(pr + col + i) = make_uint4(o[i], o[i + 1], o[i + 2], o[i + 3]);
         }
       }
     }

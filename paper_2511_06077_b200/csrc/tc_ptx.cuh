@@ -108,6 +108,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *m, const void *s
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// plain bulk copy shared -> global (TMA engine, no tensor map): bytes % 16 == 0, 16-byte aligned
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -257,16 +262,29 @@ __device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
-// 2^x for two lanes on the FMA/ALU pipes (ex2_fma below, packed); x already clamped to >= -126
+// 2^x for two lanes on the FMA/ALU pipes (ex2_fma above, packed); x already clamped to >= -126.
+// 6 packed FMA-pipe ops + 2 IMAD: j = rint(x) from the 1.5*2^23 trick, f = x - j by an FFMA2,
+// 2^j added to the exponent field as t_bits * 2^23 (the magic's own bits shift out of the word).
 __device__ __forceinline__ uint64_t ex2_fma2(uint64_t x) {
-  const uint64_t mag = f2_pack(12582912.f, 12582912.f), nmag = f2_pack(-12582912.f, -12582912.f);
-  const uint64_t t = f2_add(x, mag);
-  const uint64_t f = f2_add(x, f2_add(t, nmag) ^ 0x8000000080000000ull);  // x - rint(x)
+  const uint64_t t = f2_add(x, f2_pack(12582912.f, 12582912.f));                    // 1.5 * 2^23 + j
+  const uint64_t j = f2_add(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2_fma(j, f2_pack(-1.f, -1.f), x);                             // x - j, exact
   uint64_t p = f2_fma(f2_pack(0.05500802f, 0.05500802f), f, f2_pack(0.24220887f, 0.24220887f));
   p = f2_fma(p, f, f2_pack(0.69328306f, 0.69328306f));
   p = f2_fma(p, f, f2_pack(1.0f, 1.0f));
-  const uint32_t lo = (uint32_t)p + ((uint32_t)t << 23), hi = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
-  return (uint64_t)lo | ((uint64_t)hi << 32);
+  uint64_t r;  // per 32-bit lane: p_bits + t_bits * 2^23 (two IMADs; plain C++ here became 64-bit shifts)
+  asm("{\n .reg .b32 tl, th, pl, ph;\n mov.b64 {tl, th}, %1;\n mov.b64 {pl, ph}, %2;\n"
+      " mad.lo.u32 pl, tl, 8388608, pl;\n mad.lo.u32 ph, th, 8388608, ph;\n mov.b64 %0, {pl, ph};\n}"
+      : "=l"(r)
+      : "l"(t), "l"(p));
+  return r;
+}
+
+// three-input max (sm_100a FMNMX3): halves the instructions of a row-max reduction
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {

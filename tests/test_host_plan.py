@@ -133,6 +133,23 @@ def test_lpt_shards_match_reference():
             assert set(got.tolist()) <= set(range(P))
 
 
+def test_persistent_schedule_is_a_partition():
+    """stca_plan_persistent: every work item exactly once, CTA c's items are those LPT put in bin c,
+    in descending cost; the bins are the stca_plan_shards (LPT) assignment."""
+    rng = np.random.default_rng(5)
+    for n_ctas in (1, 3, 148):
+        for _ in range(10):
+            cost = rng.integers(1, 40, size=int(rng.integers(1, 2000)))
+            off, lst, bins = stca.plan_persistent(cost, n_ctas)
+            assert off[0] == 0 and off[-1] == len(cost) and np.all(np.diff(off) >= 0)
+            assert sorted(lst.tolist()) == list(range(len(cost)))
+            assert bins.tolist() == lpt_reference(cost.tolist(), n_ctas)
+            for c in range(n_ctas):
+                mine = lst[off[c]:off[c + 1]]
+                assert np.all(bins[mine] == c)
+                assert np.all(np.diff(cost[mine]) <= 0)
+
+
 @pytest.mark.parametrize("cap", [128, 1280, 4096])
 def test_split_history_ownership_partitions_keys(cap):
     """Split-history (PAR3): ranks own contiguous, disjoint, whole-chunk key ranges covering [0, L)."""
