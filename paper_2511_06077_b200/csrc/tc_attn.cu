@@ -58,8 +58,7 @@ constexpr int AT_PSTRIDE = AT_D + 4;           // partial row: O[d] | m | l | pa
 constexpr int AT_YSTRIDE = AT_D * 2 + 16;      // staged Y row (bytes, padded: conflict-free)
 constexpr int AT_STAGE_BYTES = AT_BM * AT_PSTRIDE * 4;  // 66 KB epilogue staging; U tile at its start
 constexpr int AT_MAXI = 128;                  // work items of a CTA cached in shared memory
-constexpr int AT_SMEM = 1024 + AT_STAGES * AT_X_BYTES + AT_STAGE_BYTES + 2 * AT_NP * 128 * 4 + AT_NP * 128 * 4 +
-                        AT_MAXI * (int)sizeof(AttnItem) + 256;
+constexpr int AT_SMEM = 1024 + AT_STAGES * AT_X_BYTES + AT_STAGE_BYTES + AT_MAXI * (int)sizeof(AttnItem) + 256;
 constexpr float AT_RESCALE_THRESHOLD = 8.f;    // log2(256)
 constexpr int AT_WP = AT_NSW, AT_WS = AT_NSW + 1, AT_WO = AT_NSW + 2, AT_THREADS = 32 * (AT_NSW + 3);
 constexpr uint32_t AT_TS = 0, AT_TO = 256, AT_TU = 384;  // TMEM columns: S0 | S1 | O | U0 | U1
@@ -77,9 +76,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sX = smem;
   uint8_t *sStage = sX + AT_STAGES * AT_X_BYTES;  // epilogue staging; the next U tile lands at its start
-  float *sMax = reinterpret_cast<float *>(sStage + AT_STAGE_BYTES);  // [tile parity][part][row]
-  float *sSum = sMax + 2 * AT_NP * 128;                               // [part][row]
-  AttnItem *sItem = reinterpret_cast<AttnItem *>(sSum + AT_NP * 128);  // this CTA's first AT_MAXI items
+  AttnItem *sItem = reinterpret_cast<AttnItem *>(sStage + AT_STAGE_BYTES);  // this CTA's first AT_MAXI items
   uint64_t *bar = reinterpret_cast<uint64_t *>(sItem + AT_MAXI);
   uint64_t *x_full = bar;                    // AT_STAGES (TMA tx)
   uint64_t *x_empty = x_full + AT_STAGES;    // AT_STAGES (S issuer: PV of the slot's tile done)
@@ -204,15 +201,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
     }
   } else {  // -------- softmax / correction / epilogue: AT_NSW warps, one row x AT_CW key columns each --------
-    const int q = warp & 3, pp = warp >> 2;  // TMEM lane quarter, key-column part
-    const int row = q * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    // U(k) (staged by TMA, SW128) -> TMEM U[k & 1] as packed bf16 pairs: this thread's AT_CW of d columns
+    // 16x32bx2 TMEM access (tools/tmem_layout): warp w owns the 16 rows 32 (w % 4) + 16 (w / 4) + t of
+    // its lane quarter; lane t < 16 and lane t + 16 share row t, holding key / O / U columns
+    // [0, 64) and [64, 128) of it (pp = lane / 16).  The row max of a tile is one shuffle: the warps
+    // never wait for each other inside a tile (no shared-memory exchange, no named barrier).
+    const int pp = lane >> 4;
+    const int row = (warp & 3) * 32 + (warp >> 2) * 16 + (lane & 15);
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32 + (warp >> 2) * 16) << 16;
+    // U(k) (staged by TMA, SW128) -> TMEM U[k & 1] as packed bf16 pairs: this thread's 64 of d columns
     auto load_u = [&](int k) {
       mbar_wait(us_full, k & 1);
       const uint8_t *box = sStage + pp * (AT_U_BYTES / 2);  // pp = 64-column half of d
 #pragma unroll
-      for (int h16 = 0; h16 < AT_CW / 32; ++h16) {  // 32 bf16 = 16 packed columns per store
+      for (int h16 = 0; h16 < 2; ++h16) {  // 32 bf16 = 16 packed columns per store
         uint32_t w[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           w[4 * c + 2] = v.z;
           w[4 * c + 3] = v.w;
         }
-        tmem_st16(tmem + lane_off + AT_TU + (k & 1) * 64 + (AT_CW / 2) * pp + 16 * h16, w);
+        tmem_st16x2_16<32>(tmem + lane_off + AT_TU + (k & 1) * 64 + 16 * h16, w);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -233,48 +234,42 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
     };
     if (ni > 0) load_u(0);
-    int jj = 0;               // global tile counter
+    int jj = 0;                 // global tile counter
     bool bulk_pending = false;  // warp 0: an item's output copy may still be reading the staging
     for (int k = 0; k < ni; ++k) {
       const AttnItem it = item(k);
       const int nt = (it.klen + AT_BN - 1) / AT_BN;
-      float m = -INFINITY, l = 0.f;  // l: this part's share of the row sum
+      float m = -INFINITY, l = 0.f;  // l: this thread's half of the row sum
       for (int j = 0; j < nt; ++j, ++jj) {
         const int b = jj & 1;
         mbar_wait(&s_full[b], (jj >> 1) & 1);
         if (warp == 0 && lane == 0) AT_TR(jj * 16 + 6);
         tc_fence_after();
-        const int kvalid = it.klen - j * AT_BN - AT_CW * pp;  // keys of this part inside the chunk
+        const int kvalid = it.klen - j * AT_BN - AT_CW * pp;  // keys of this half inside the chunk
         uint32_t sr[AT_CW];
-#pragma unroll
-        for (int c = 0; c < AT_CW; c += 32)
-          tmem_ld32(tmem + lane_off + AT_TS + b * AT_BN + AT_CW * pp + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
+        tmem_ld16x2_32<64>(tmem + lane_off + AT_TS + b * AT_BN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        tmem_ld16x2_32<64>(tmem + lane_off + AT_TS + b * AT_BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         tmem_ld_wait();
-        float mx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-        const bool partial = kvalid < AT_CW;  // warp-uniform: only a chunk's last tile needs the mask
+        const bool partial = it.klen - j * AT_BN < AT_BN;  // warp-uniform: only a chunk's last tile is masked
         if (partial) {
 #pragma unroll
           for (int c = 0; c < AT_CW; ++c)
             if (c >= kvalid) sr[c] = __float_as_uint(-INFINITY);
         }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
 #pragma unroll
         for (int c = 0; c < AT_CW; c += 2)
           mx[(c >> 1) & 7] = fmax3(mx[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-        sMax[(b * AT_NP + pp) * 128 + row] = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                                   fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        float mt = fmaxf(fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5])), fmaxf(mx[6], mx[7]));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 16));  // the row's other half
         if (warp == 0 && lane == 0) AT_TR(jj * 16 + 7);
-        named_bar_sync(1, 32 * AT_NSW);  // every part's S columns are in registers and its maximum posted
-        if (warp == 0 && lane == 0) AT_TR(jj * 16 + 8);
-        float mt = sMax[(b * AT_NP) * 128 + row];
-#pragma unroll
-        for (int kk = 1; kk < AT_NP; ++kk) mt = fmaxf(mt, sMax[(b * AT_NP + kk) * 128 + row]);
         const bool need = mt > m + AT_RESCALE_THRESHOLD;
         if (j == 0) {
           m = mt;
         } else if (__any_sync(0xffffffffu, need)) {
-          // warp-uniform: this part of O *= 2^(m - m_new) per row once every PV issued so far has landed
+          // warp-uniform: O *= 2^(m - m_new) per row once every PV issued so far has landed
           mbar_wait(&pv_done[(jj - 1) & 1], ((jj - 1) >> 1) & 1);
           tc_fence_after();
           const float mnew = need ? mt : m;
@@ -283,19 +278,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll 1
           for (int c = 0; c < AT_CW; c += 16) {
             uint32_t o[16];
-            tmem_ld16(tmem + lane_off + AT_TO + AT_CW * pp + c, o);
+            tmem_ld16x2_16<64>(tmem + lane_off + AT_TO + c, o);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
-            tmem_st16(tmem + lane_off + AT_TO + AT_CW * pp + c, o);
+            tmem_st16x2_16<64>(tmem + lane_off + AT_TO + c, o);
           }
           tmem_st_wait();
           m = mnew;
         }
-        // P = 2^(S - m) as bf16 pairs: keys [AT_CW pp, AT_CW (pp + 1)) -> S buffer b columns
-        // [AT_CW/2 pp, AT_CW/2 (pp + 1)).  Packed fp32x2 arithmetic; on full tiles 3 of every 8 pairs
-        // of exponentials run on the FMA pipe (ex2_fma2): at d = 128 one exp per (row, key) balances
-        // MUFU and the tensor pipe exactly.  The row sum accumulates the fp32 values.
+        // P = 2^(S - m) as bf16 pairs: this thread's 64 keys -> S buffer b packed columns [32 pp, 32 pp + 32).
+        // Packed fp32x2 arithmetic; on full tiles 3 of every 8 pairs of exponentials run on the FMA
+        // pipe (ex2_fma2): at d = 128 one exp per (row, key) balances MUFU and the tensor pipe exactly.
+        // The row sum accumulates the fp32 values.
         const uint64_t nm2 = f2_pack(-m, -m);
         uint64_t ls2[2] = {0ull, 0ull};
         uint32_t w[AT_CW / 2];
@@ -322,9 +317,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
         const uint64_t lsum = f2_add(ls2[0], ls2[1]);
         if (warp == 0 && lane == 0) AT_TR(jj * 16 + 12);
-#pragma unroll
-        for (int c = 0; c < AT_CW / 2; c += 16)
-          tmem_st16(tmem + lane_off + AT_TS + b * AT_BN + (AT_CW / 2) * pp + c, *reinterpret_cast<uint32_t(*)[16]>(&w[c]));
+        tmem_st16x2_16<32>(tmem + lane_off + AT_TS + b * AT_BN, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+        tmem_st16x2_16<32>(tmem + lane_off + AT_TS + b * AT_BN + 16, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
         l += f2_lo(lsum) + f2_hi(lsum);
         tmem_st_wait();
         if (warp == 0 && lane == 0) AT_TR(jj * 16 + 13);
@@ -350,18 +344,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_wait(&pv_done[(jj - 1) & 1], ((jj - 1) >> 1) & 1);
       AT_TRE(0);
       tc_fence_after();
-      sSum[pp * 128 + row] = l;
-      named_bar_sync(1, 32 * AT_NSW);  // sums posted; every warp is past its U copy (staging is free)
+      const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);  // the row's two halves
+      named_bar_sync(1, 32 * AT_NSW);  // every warp is past its U copy: the staging area is free
       AT_TRE(1);
-      float lrow = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < AT_NP; ++kk) lrow += sSum[kk * 128 + row];
       const bool single = it.part_row < 0;
       const float inv = 1.f / lrow;
 #pragma unroll 1
       for (int cb = 0; cb < AT_CW; cb += 32) {
         uint32_t o[32];
-        tmem_ld32(tmem + lane_off + AT_TO + AT_CW * pp + cb, o);
+        tmem_ld16x2_32<64>(tmem + lane_off + AT_TO + cb, o);
         tmem_ld_wait();
         if (single) {
           uint8_t *dst = sStage + row * AT_YSTRIDE + (AT_CW * pp + cb) * 2;
