@@ -121,6 +121,13 @@ stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const
 stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                          float *out_Z, float *out_z, void *stream);
 
+/* The projected history cache of the last stca_project_history, Eq.(2): rows [row0, row0 + nrows)
+ * of X~(layer), layer = 1..M, in compacted cache order (request b's kept rows start at the sum of
+ * the kept lengths L'_{b'} of the requests before it), widened to float32 into out [nrows x d]
+ * (device or host; a host copy completes before return).  STATE before any projection,
+ * INVALID_ARG for a layer or row range outside the cache. */
+stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t row0, int64_t nrows, float *out, void *stream);
+
 void stca_destroy(stca_handle *h);                  /* NULL-safe; synchronises the device */
 const char *stca_last_error(const stca_handle *h);  /* last non-OK message; h == NULL: last failed create on this thread */
 const char *stca_status_string(int32_t status);

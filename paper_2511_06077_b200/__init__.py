@@ -142,6 +142,17 @@ class STCA:
                                                 ctypes.c_void_p(_stream(stream))))
         self._B = B
 
+    def read_cache(self, layer: int, row0: int = 0, nrows: Optional[int] = None, out=None, stream=None):
+        """Rows of the projected X~(layer) cache (compacted order) as float32; returns `out` (a new host
+        array [nrows, d] unless a device or host buffer is given)."""
+        if nrows is None:
+            raise ValueError("nrows is required (the cache holds sum_b L'_b rows)")
+        if out is None:
+            out = np.empty((nrows, self.d), dtype=np.float32)
+        self._check(lib().stca_read_cache(self._h, int(layer), int(row0), int(nrows), ctypes.c_void_p(_ptr(out)),
+                                          ctypes.c_void_p(_stream(stream))))
+        return out
+
     def forward(self, xt, tgt_off, out_Z, out_z=None, stream=None, sync=None) -> None:
         """Eq.(3)-(9) for the targets of the projected requests; writes out_Z [Nt,M,d], out_z [Nt,d].
 

@@ -752,6 +752,42 @@ static stca_status gemm(stca_handle *h, const void *A, int64_t lda, const void *
   return STCA_OK;
 }
 
+// ===========================================================================
+// read back the projected cache (inspection / tests of the history path alone)
+// ===========================================================================
+extern "C" stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t row0, int64_t nrows, float *out,
+                                       void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a failed state: %s", h->err.c_str());
+  if (h->B < 0) return fail(h, STCA_ERR_STATE, "read_cache before project_history");
+  if (layer < 1 || layer > h->cfg.M) return fail(h, STCA_ERR_INVALID_ARG, "layer %d outside 1..%d", layer, h->cfg.M);
+  if (row0 < 0 || nrows < 0 || row0 + nrows > h->T2)
+    return fail(h, STCA_ERR_INVALID_ARG, "rows [%lld, %lld) outside the cache's %lld rows", (long long)row0,
+                (long long)(row0 + nrows), (long long)h->T2);
+  if (nrows == 0) return STCA_OK;
+  if (!out) return fail(h, STCA_ERR_INVALID_ARG, "out is NULL");
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = h->cfg.d;
+  const size_t n = (size_t)nrows * d;
+  const uint8_t *src = (const uint8_t *)h->xt_cache.p + ((size_t)(layer - 1) * h->T2 + row0) * d * h->es;
+  const bool host = !is_device_ptr(out);
+  float *dst = out;
+  if (host) {
+    CU(h->Zout.ensure(n * 4));
+    dst = h->Zout.as<float>();
+  }
+  if (h->bf16)
+    CU(stca::bf16_to_f32((const stca::bf16 *)src, dst, (int64_t)n, st));
+  else
+    CU(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, st));
+  if (host) {
+    CU(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));  // the scratch buffer is reused by forward
+  }
+  return STCA_OK;
+}
+
 extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                                     float *out_Z, float *out_z, void *stream) {
   if (!h) return STCA_ERR_INVALID_ARG;

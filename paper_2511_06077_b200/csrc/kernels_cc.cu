@@ -363,6 +363,20 @@ cudaError_t f32_to_bf16(const float *src, bf16 *dst, int64_t n, cudaStream_t st)
   return cudaGetLastError();
 }
 
+__global__ void k_bf16_to_f32(const bf16 *__restrict__ s, float *__restrict__ t, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    t[i] = __bfloat162float(s[i]);
+}
+
+cudaError_t bf16_to_f32(const bf16 *src, float *dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  unsigned g = (unsigned)((n + 255) / 256);
+  if (g > 8192) g = 8192;
+  note_launch();
+  k_bf16_to_f32<<<g, 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
 // W_QK^r = W_Q^r W_K^r^T (scaled) and W_VO^r = W_V^r W_O^r, one thread per output element.
 __global__ void k_prep_qk_vo(const float *__restrict__ WQ, const float *__restrict__ WK,
                              const float *__restrict__ WV, const float *__restrict__ WO, int d, int h, float scale,
