@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chunk-keys", type=int, default=0, help="split-K chunk cap in keys (0: library default)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     args.gpus = max(args.gpus, world)
@@ -197,7 +198,7 @@ def main():
     W = workload.full_weights(workload.make_workload(args.config, seed=args.seed, B=1)) if rank else \
         workload.full_weights(wl)                                            # weights replicated (seed 0 draw)
     model = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, dtype=c.dtype, with_z=c.with_z,
-                      device=local, chunk_keys=1280 if split else 0,
+                      device=local, chunk_keys=1280 if split else args.chunk_keys,
                       split_rank=rank if split else 0, split_world=world if split else 1,
                       exchange=stca.nccl_exchange() if split and world > 1 else None)
     bf16 = c.dtype == "bf16"

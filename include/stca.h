@@ -59,7 +59,7 @@ typedef struct {
   int32_t dtype;          /* stca_dtype */
   int32_t with_z;         /* also compute z = SwiGLUFFN_Z([o(1)..o(M)|x_t] W_Z), Eq.(9) */
   int32_t device;         /* CUDA ordinal the handle lives on */
-  int32_t chunk_keys;     /* split-K chunk length cap in keys (multiple of 128); 0 = default 4096 */
+  int32_t chunk_keys;     /* split-K chunk length cap in keys (multiple of 128); 0 = default 8192 */
   int32_t split_rank;     /* split-history mode: this rank, 0..split_world-1 */
   int32_t split_world;    /* 1 = off; > 1: every rank gets the SAME full inputs and owns a */
                           /* contiguous block of key chunks of every history */

@@ -16,6 +16,9 @@
 #include "tc.h"
 
 #define STCA_H2D_PIECES 8  // pieces of a pipelined host-input projection
+// default split-K chunk cap: a 10k history runs as 2 chunks (measured: 4096 -> 3 chunks cost the serve
+// forward ~9% more in partial traffic and merge; no split at all balances the persistent grid worse)
+#define STCA_DEFAULT_CHUNK_KEYS 8192
 
 using stca::bf16;
 
@@ -102,7 +105,7 @@ struct stca_handle {
   // forward scratch
   DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, ctal, zout, Zout;
   HostPinned pin;
-  int64_t chunk_cap = 4096;
+  int64_t chunk_cap = STCA_DEFAULT_CHUNK_KEYS;
   // pipelined host-input projection: copy stream + one event per piece
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_xin_free = nullptr, ev[STCA_H2D_PIECES] = {};
@@ -202,7 +205,7 @@ void stca_plan_suffix(const int64_t *hist_off, int64_t B, int32_t L_infer, int64
 }
 
 int32_t stca_plan_chunks(int64_t L, int32_t chunk_keys, int64_t *chunk_len) {
-  const int64_t cap = chunk_keys > 0 ? chunk_keys : 4096;
+  const int64_t cap = chunk_keys > 0 ? chunk_keys : STCA_DEFAULT_CHUNK_KEYS;
   if (L <= 0) {
     if (chunk_len) *chunk_len = 0;
     return 0;
@@ -367,7 +370,7 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
   if (h->cfg.split_world == 0) h->cfg.split_world = 1;
   h->bf16 = cfg->dtype == STCA_BF16;
   h->es = h->bf16 ? 2 : 4;
-  h->chunk_cap = cfg->chunk_keys > 0 ? cfg->chunk_keys : 4096;
+  h->chunk_cap = cfg->chunk_keys > 0 ? cfg->chunk_keys : STCA_DEFAULT_CHUNK_KEYS;
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     cudaGetLastError();
     return bad(fail(h, STCA_ERR_CUDA, "cudaSetDevice(%d) failed", cfg->device));

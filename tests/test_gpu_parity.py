@@ -59,6 +59,14 @@ def test_ragged_multichunk_suffix(dtype):
     check(wl, Z, z, TOL[dtype])
 
 
+def test_ragged_many_chunks_bf16():
+    """chunk_keys = 1280: the 9000-key history splits into 8 chunks (the cap C <= 8), 4097 / 5000 into 4;
+    split-K partials and the LSE merge on every multi-chunk request."""
+    wl = ragged_workload("bf16")
+    Z, z = run_gpu(wl, chunk_keys=1280)
+    check(wl, Z, z, TOL["bf16"])
+
+
 @pytest.mark.parametrize("d,h", [(64, 2), (256, 8)])
 def test_bf16_other_widths(d, h):
     wl = ragged_workload("bf16", d=d, h=h, M=3, L_infer=0)

@@ -78,7 +78,7 @@ def test_suffix_matches_oracle_bit_exact():
 def test_chunks_partition(cap):
     for L in [1, 2, 127, 128, 129, 1000, 4095, 4096, 4097, 8192, 8193, 10000, 12345, 40000]:
         n, cl = stca.plan_chunks(L, cap)
-        capv = cap or 4096
+        capv = cap or 8192
         assert cl % 128 == 0 and cl > 0
         assert (n - 1) * cl < L <= n * cl                      # every chunk non-empty, union = [0, L)
         assert cl <= capv or n == 1 or cl <= ((capv + 127) // 128) * 128
