@@ -6,7 +6,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstca.so")
+# STCA_LIB: another in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("STCA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstca.so")
 STCA_BF16, STCA_FP32 = 0, 1
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
