@@ -247,12 +247,15 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
   int64_t off[MAXC];
   float w[MAXC];
   float2 ml[MAXC];  // (m, l) of every chunk: one 8-byte load each, all issued before any use
+  float4 a0[MAXC];  // and the first 128 O columns of every chunk (no dependence on the weights)
   float mu = -INFINITY;
+  const int e0 = lane * 4;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (c < it.nchunks) {
       off[c] = (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride;
       ml[c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d));
+      if (e0 < d) a0[c] = __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e0));
     }
   }
 #pragma unroll
@@ -267,12 +270,12 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
     }
   }
   const float inv = 1.f / l;
-  for (int e = lane * 4; e < d; e += 128) {  // d % 4 == 0: 16-B vector loads of the O rows
+  for (int e = e0; e < d; e += 128) {  // d % 4 == 0: 16-B vector loads of the O rows
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c < it.nchunks) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e));  // 16-byte rows
+        const float4 a = e == e0 ? a0[c] : __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e));
         acc.x += w[c] * a.x;
         acc.y += w[c] * a.y;
         acc.z += w[c] * a.z;

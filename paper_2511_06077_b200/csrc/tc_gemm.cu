@@ -121,6 +121,9 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(tfull);
     }
   } else {  // epilogue warps 0..3: TMEM lane quarter = warp
+    // Results are staged in shared memory (the pipeline stages are idle once tfull fires) with
+    // padded rows, then copied out by all 128 threads with coalesced 16-byte stores: a row per
+    // thread written straight to global touches 32 sectors per store instruction.
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int64_t grow = (int64_t)m0 + row;
@@ -128,28 +131,61 @@ __global__ void __launch_bounds__(192, 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr int F_STRIDE = 32 * 4 + 16;   // staged fp32 row of a 32-column block (bytes)
+    constexpr int H_STRIDE = 32 * 2 + 16;   // staged bf16 row of a 32-column block
+    constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of this tile
+    constexpr int NB = OUT_COLS / 32 > 0 ? OUT_COLS / 32 : 1;     // 32-column blocks
+    constexpr int NBG_ = (C::STAGES * C::STAGE) / (128 * F_STRIDE);  // blocks per staging round
+    constexpr int NBG = NBG_ < NB ? NBG_ : NB;
+    static_assert(NBG >= 1, "one staged block fits the idle pipeline stages");
+    uint8_t *stg = smem;
+    const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
+    // cooperative copy of the staged blocks [blk0, blk0 + nb) (row stride RS bytes, BW bytes per
+    // block row) to dst (row stride ld elements of ES bytes)
+    auto copy_out = [&](int blk0, int nb, int RS, int BW, uint8_t *dst, int64_t ld, int ES) {
+      named_bar_sync(1, 128);
+      const int per_row = BW / 16, per_blk = 128 * per_row;
+      for (int i = threadIdx.x; i < nb * per_blk; i += 128) {
+        const int blk = i / per_blk, rr = (i % per_blk) / per_row, ch = i % per_row;
+        if ((int64_t)m0 + rr < M)
+          *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + out_n0 + (blk0 + blk) * 32) * ES + ch * 16) =
+              *reinterpret_cast<const uint4 *>(stg + (blk * 128 + rr) * RS + ch * 16);
+      }
+      named_bar_sync(1, 128);  // the staging may be rewritten
+    };
+    auto stage_f32 = [&](int blk, const float (&y)[32]) {
+      uint8_t *dst = stg + ((blk % NBG) * 128 + row) * F_STRIDE;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float4 *>(dst + 16 * i) = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+    };
+    auto stage_bf16 = [&](int blk, const float (&y)[32]) {
+      uint8_t *dst = stg + ((blk % NBG) * 128 + row) * H_STRIDE;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<uint4 *>(dst + 16 * i) =
+            make_uint4(pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
+                       pack_bf16(y[8 * i + 4], y[8 * i + 5]), pack_bf16(y[8 * i + 6], y[8 * i + 7]));
+    };
     if (EPI == TEPI_STORE) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c, r);
-        tmem_ld_wait();
-        if (ok) {
-          if (ea.Cf) {
-            float4 *dst = reinterpret_cast<float4 *>(ea.Cf + grow * ea.ldcf + n0 + c);
+      for (int pass = 0; pass < 2; ++pass) {  // fp32 output, then bf16 output (either may be absent)
+        if (pass == 0 ? !ea.Cf : !ea.Cs) continue;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
+          float y[32];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              dst[i] = make_float4(alpha * __uint_as_float(r[4 * i]), alpha * __uint_as_float(r[4 * i + 1]),
-                                   alpha * __uint_as_float(r[4 * i + 2]), alpha * __uint_as_float(r[4 * i + 3]));
-          }
-          if (ea.Cs) {
-            uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + n0 + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pack_bf16(alpha * __uint_as_float(r[8 * i]), alpha * __uint_as_float(r[8 * i + 1])),
-                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 2]), alpha * __uint_as_float(r[8 * i + 3])),
-                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 4]), alpha * __uint_as_float(r[8 * i + 5])),
-                                  pack_bf16(alpha * __uint_as_float(r[8 * i + 6]), alpha * __uint_as_float(r[8 * i + 7])));
+          for (int i = 0; i < 32; ++i) y[i] = alpha * __uint_as_float(r[i]);
+          const int blk = c / 32;
+          if (pass == 0) stage_f32(blk, y);
+          else stage_bf16(blk, y);
+          if (blk % NBG == NBG - 1 || blk == NB - 1) {
+            const int b0 = blk - blk % NBG;
+            if (pass == 0) copy_out(b0, blk - b0 + 1, F_STRIDE, 128, reinterpret_cast<uint8_t *>(ea.Cf), ea.ldcf, 4);
+            else copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
           }
         }
       }
@@ -160,19 +196,14 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(taddr + c, u);
         tmem_ld32(taddr + c + 32, v);
         tmem_ld_wait();
-        if (ok) {
-          uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + (n0 + c) / 2);
+        float y[32];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t w[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int e = 8 * i + 2 * j;
-              w[j] = pack_bf16(__uint_as_float(u[e]) * silu_f(__uint_as_float(v[e])),
-                               __uint_as_float(u[e + 1]) * silu_f(__uint_as_float(v[e + 1])));
-            }
-            dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
+        for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(u[e]) * silu_f(__uint_as_float(v[e]));
+        const int blk = c / 64;
+        stage_bf16(blk, y);
+        if (blk % NBG == NBG - 1 || blk == NB - 1) {
+          const int b0 = blk - blk % NBG;
+          copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
         }
       }
     } else {  // TEPI_LN over BN == d columns
@@ -200,29 +231,28 @@ __global__ void __launch_bounds__(192, 1)
       }
       const float inv = rsqrtf(v2 / BN + ea.eps);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c, r);
-        tmem_ld_wait();
-        if (ok) {
+      for (int pass = 0; pass < 2; ++pass) {  // fp32 output, then bf16 output
+        if (pass == 0 ? !ea.Cf : !ea.Cs) continue;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
           float y[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) y[i] = (__uint_as_float(r[i]) - mu) * inv * __ldg(ea.g + c + i) + __ldg(ea.b + c + i);
-          if (ea.Cs) {
-            uint4 *dst = reinterpret_cast<uint4 *>(ea.Cs + grow * ea.ldcs + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
-                                  pack_bf16(y[8 * i + 4], y[8 * i + 5]), pack_bf16(y[8 * i + 6], y[8 * i + 7]));
-          }
-          if (ea.Cf) {
-            float4 *dst = reinterpret_cast<float4 *>(ea.Cf + grow * ea.ldcf + c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) dst[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+          const int blk = c / 32;
+          if (pass == 0) stage_f32(blk, y);
+          else stage_bf16(blk, y);
+          if (blk % NBG == NBG - 1 || blk == NB - 1) {
+            const int b0 = blk - blk % NBG;
+            if (pass == 0) copy_out(b0, blk - b0 + 1, F_STRIDE, 128, reinterpret_cast<uint8_t *>(ea.Cf), ea.ldcf, 4);
+            else copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
           }
         }
       }
     }
+    (void)ok;
   }
   tc_fence_before();
   __syncthreads();
