@@ -17,6 +17,7 @@
 #include <math.h>
 #include <stdio.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "launch.h"
@@ -48,11 +49,20 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
+  static constexpr int F_STRIDE = 32 * 4 + 16;    // staged fp32 row of a 32-column output block (bytes)
+  static constexpr int H_STRIDE = 32 * 2 + 16;    // staged bf16 row
+  static constexpr int STG_BYTES = 128 * F_STRIDE;  // one staged output block (dedicated: the ring keeps running)
+  static constexpr int STAGES = (196 * 1024 / STAGE) > 4 ? 4 : (196 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int NACC = TMEM_COLS <= 256 ? 2 : 1;  // TMEM accumulators (double-buffered when they fit)
+  static constexpr int SMEM = STAGES * STAGE + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// PERSISTENT: grid = min(tiles, SMs); CTA c takes output tiles c, c + grid, ... (m fastest).  The
+// smem ring runs across tiles and the TMEM accumulator is double-buffered, so the epilogue of tile
+// i (TMEM -> registers -> padded smem block -> coalesced 16-byte stores) overlaps the MMAs of tile
+// i+1 and the loads of tile i+2; per-tile launch / prologue / pipeline-fill costs are paid once
+// per SM instead of once per tile (these GEMMs are small: M = N_t = 16384 rows).
 template <int BN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
@@ -60,13 +70,15 @@ __global__ void __launch_bounds__(192, 1)
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE);
+  uint8_t *stg = smem + C::STAGES * C::STAGE;
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + C::STG_BYTES);
   uint64_t *empty = full + C::STAGES;
-  uint64_t *tfull = empty + C::STAGES;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(tfull + 1);
+  uint64_t *acc_full = empty + C::STAGES;   // NACC (MMA commit: accumulator a complete)
+  uint64_t *acc_empty = acc_full + 2;       // NACC (4 epilogue warps: accumulator a read)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
+  const int tiles_m = (M + C::BM - 1) / C::BM, ntiles = tiles_m * (N / BN);
   const int nk = (K + C::BK - 1) / C::BK;
 
   if (warp == 4 && lane == 0) {
@@ -76,10 +88,13 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tslot, C::TMEM_COLS);
+  if (warp == 5) tmem_alloc(tslot, C::NACC * C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -87,90 +102,92 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 4) {
     if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t *sa = smem + s * C::STAGE, *sb = sa + C::A_BYTES;
-        mbar_expect_tx(&full[s], C::STAGE);
-        tma_load_2d(sa, &mapA, &full[s], kb * C::BK, m0);
+      int s = 0, ph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % tiles_m) * C::BM, n0 = (t / tiles_m) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *sa = smem + s * C::STAGE, *sb = sa + C::A_BYTES;
+          mbar_expect_tx(&full[s], C::STAGE);
+          tma_load_2d(sa, &mapA, &full[s], kb * C::BK, m0);
 #pragma unroll
-        for (int j = 0; j < BN / C::NS; ++j) tma_load_2d(sb + j * C::NS * 128, &mapB, &full[s], kb * C::BK, n0 + j * C::NS);
+          for (int j = 0; j < BN / C::NS; ++j)
+            tma_load_2d(sb + j * C::NS * 128, &mapB, &full[s], kb * C::BK, n0 + j * C::NS);
+          if (++s == C::STAGES) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 5) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = idesc_bf16(128, C::NS, 0);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int s = 0, ph = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int a = i % C::NACC;
+        mbar_wait(&acc_empty[a], ((i / C::NACC) & 1) ^ 1);  // the epilogue has read this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * C::STAGE), sb = sa + C::A_BYTES;
+        const uint32_t acc = tmem + a * C::TMEM_COLS;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * C::STAGE), sb = sa + C::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
+          for (int k = 0; k < C::BK / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
 #pragma unroll
-          for (int j = 0; j < BN / C::NS; ++j) {
-            const uint64_t bd = sdesc_sw128(sb + j * C::NS * 128 + k * 32, 16, 1024);
-            umma_f16_ss(tmem + j * C::NS, ad, bd, idesc, (kb | k) != 0);
+            for (int j = 0; j < BN / C::NS; ++j) {
+              const uint64_t bd = sdesc_sw128(sb + j * C::NS * 128 + k * 32, 16, 1024);
+              umma_f16_ss(acc + j * C::NS, ad, bd, idesc, (kb | k) != 0);
+            }
           }
+          umma_commit(&empty[s]);
+          if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
-        umma_commit(&empty[s]);
+        umma_commit(&acc_full[a]);
       }
-      umma_commit(tfull);
     }
   } else {  // epilogue warps 0..3: TMEM lane quarter = warp
-    // Results are staged in shared memory (the pipeline stages are idle once tfull fires) with
-    // padded rows, then copied out by all 128 threads with coalesced 16-byte stores: a row per
-    // thread written straight to global touches 32 sectors per store instruction.
+    // Each 32-column output block is staged in shared memory with padded rows, then copied out by
+    // all 128 threads with coalesced 16-byte stores (a row per thread written straight to global
+    // touches 32 sectors per store instruction).
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int64_t grow = (int64_t)m0 + row;
-    const bool ok = grow < M;
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
-    constexpr int F_STRIDE = 32 * 4 + 16;   // staged fp32 row of a 32-column block (bytes)
-    constexpr int H_STRIDE = 32 * 2 + 16;   // staged bf16 row of a 32-column block
-    constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of this tile
-    constexpr int NB = OUT_COLS / 32 > 0 ? OUT_COLS / 32 : 1;     // 32-column blocks
-    constexpr int NBG_ = (C::STAGES * C::STAGE) / (128 * F_STRIDE);  // blocks per staging round
-    constexpr int NBG = NBG_ < NB ? NBG_ : NB;
-    static_assert(NBG >= 1, "one staged block fits the idle pipeline stages");
-    uint8_t *stg = smem;
-    const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
-    // cooperative copy of the staged blocks [blk0, blk0 + nb) (row stride RS bytes, BW bytes per
-    // block row) to dst (row stride ld elements of ES bytes)
-    auto copy_out = [&](int blk0, int nb, int RS, int BW, uint8_t *dst, int64_t ld, int ES) {
-      named_bar_sync(1, 128);
-      const int per_row = BW / 16, per_blk = 128 * per_row;
-      for (int i = threadIdx.x; i < nb * per_blk; i += 128) {
-        const int blk = i / per_blk, rr = (i % per_blk) / per_row, ch = i % per_row;
-        if ((int64_t)m0 + rr < M)
-          *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + out_n0 + (blk0 + blk) * 32) * ES + ch * 16) =
-              *reinterpret_cast<const uint4 *>(stg + (blk * 128 + rr) * RS + ch * 16);
-      }
-      named_bar_sync(1, 128);  // the staging may be rewritten
-    };
-    auto stage_f32 = [&](int blk, const float (&y)[32]) {
-      uint8_t *dst = stg + ((blk % NBG) * 128 + row) * F_STRIDE;
+    constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int m0 = (t % tiles_m) * C::BM, n0 = (t / tiles_m) * BN;
+      const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
+      const int a = i % C::NACC;
+      mbar_wait(&acc_full[a], (i / C::NACC) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + a * C::TMEM_COLS + ((uint32_t)(q * 32) << 16);
+      // stage block `blk` (32 output columns, fp32 or bf16 rows), then store it coalesced
+      auto emit = [&](int blk, const float (&y)[32], bool f32) {
+        const int RS = f32 ? C::F_STRIDE : C::H_STRIDE, BW = f32 ? 128 : 64, ES = f32 ? 4 : 2;
+        uint8_t *srow = stg + row * RS;
+        if (f32) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        *reinterpret_cast<float4 *>(dst + 16 * i) = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
-    };
-    auto stage_bf16 = [&](int blk, const float (&y)[32]) {
-      uint8_t *dst = stg + ((blk % NBG) * 128 + row) * H_STRIDE;
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4 *>(srow + 16 * k) = make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+        } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        *reinterpret_cast<uint4 *>(dst + 16 * i) =
-            make_uint4(pack_bf16(y[8 * i], y[8 * i + 1]), pack_bf16(y[8 * i + 2], y[8 * i + 3]),
-                       pack_bf16(y[8 * i + 4], y[8 * i + 5]), pack_bf16(y[8 * i + 6], y[8 * i + 7]));
-    };
-    if (EPI == TEPI_STORE) {
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {  // fp32 output, then bf16 output (either may be absent)
-        if (pass == 0 ? !ea.Cf : !ea.Cs) continue;
+          for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<uint4 *>(srow + 16 * k) =
+                make_uint4(pack_bf16(y[8 * k], y[8 * k + 1]), pack_bf16(y[8 * k + 2], y[8 * k + 3]),
+                           pack_bf16(y[8 * k + 4], y[8 * k + 5]), pack_bf16(y[8 * k + 6], y[8 * k + 7]));
+        }
+        named_bar_sync(1, 128);
+        uint8_t *dst = f32 ? reinterpret_cast<uint8_t *>(ea.Cf) : reinterpret_cast<uint8_t *>(ea.Cs);
+        const int64_t ld = f32 ? ea.ldcf : ea.ldcs;
+        const int per_row = BW / 16;
+        for (int c = threadIdx.x; c < 128 * per_row; c += 128) {
+          const int rr = c / per_row, ch = c % per_row;
+          if ((int64_t)m0 + rr < M)
+            *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + out_n0 + blk * 32) * ES + ch * 16) =
+                *reinterpret_cast<const uint4 *>(stg + rr * RS + ch * 16);
+        }
+        named_bar_sync(1, 128);  // the staging block may be rewritten
+      };
+      if (EPI == TEPI_STORE) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
@@ -178,61 +195,46 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld_wait();
           float y[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) y[i] = alpha * __uint_as_float(r[i]);
-          const int blk = c / 32;
-          if (pass == 0) stage_f32(blk, y);
-          else stage_bf16(blk, y);
-          if (blk % NBG == NBG - 1 || blk == NB - 1) {
-            const int b0 = blk - blk % NBG;
-            if (pass == 0) copy_out(b0, blk - b0 + 1, F_STRIDE, 128, reinterpret_cast<uint8_t *>(ea.Cf), ea.ldcf, 4);
-            else copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
+          for (int e = 0; e < 32; ++e) y[e] = alpha * __uint_as_float(r[e]);
+          if (ea.Cf) emit(c / 32, y, true);
+          if (ea.Cs) emit(c / 32, y, false);
+        }
+      } else if (EPI == TEPI_SWIGLU) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          uint32_t u[32], v[32];
+          tmem_ld32(taddr + c, u);
+          tmem_ld32(taddr + c + 32, v);
+          tmem_ld_wait();
+          float y[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(u[e]) * silu_f(__uint_as_float(v[e]));
+          emit(c / 64, y, false);
+        }
+      } else {  // TEPI_LN over BN == d columns
+        float sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sum += __uint_as_float(r[e]);
+        }
+        const float mu = sum / BN;
+        float v2 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float d0 = __uint_as_float(r[e]) - mu;
+            v2 += d0 * d0;
           }
         }
-      }
-    } else if (EPI == TEPI_SWIGLU) {
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 64) {
-        uint32_t u[32], v[32];
-        tmem_ld32(taddr + c, u);
-        tmem_ld32(taddr + c + 32, v);
-        tmem_ld_wait();
-        float y[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(u[e]) * silu_f(__uint_as_float(v[e]));
-        const int blk = c / 64;
-        stage_bf16(blk, y);
-        if (blk % NBG == NBG - 1 || blk == NB - 1) {
-          const int b0 = blk - blk % NBG;
-          copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
-        }
-      }
-    } else {  // TEPI_LN over BN == d columns
-      float s = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s += __uint_as_float(r[i]);
-      }
-      const float mu = s / BN;
-      float v2 = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float t = __uint_as_float(r[i]) - mu;
-          v2 += t * t;
-        }
-      }
-      const float inv = rsqrtf(v2 / BN + ea.eps);
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {  // fp32 output, then bf16 output
-        if (pass == 0 ? !ea.Cf : !ea.Cs) continue;
+        const float inv = rsqrtf(v2 / BN + ea.eps);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
@@ -240,23 +242,21 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld_wait();
           float y[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) y[i] = (__uint_as_float(r[i]) - mu) * inv * __ldg(ea.g + c + i) + __ldg(ea.b + c + i);
-          const int blk = c / 32;
-          if (pass == 0) stage_f32(blk, y);
-          else stage_bf16(blk, y);
-          if (blk % NBG == NBG - 1 || blk == NB - 1) {
-            const int b0 = blk - blk % NBG;
-            if (pass == 0) copy_out(b0, blk - b0 + 1, F_STRIDE, 128, reinterpret_cast<uint8_t *>(ea.Cf), ea.ldcf, 4);
-            else copy_out(b0, blk - b0 + 1, H_STRIDE, 64, reinterpret_cast<uint8_t *>(ea.Cs), ea.ldcs, 2);
-          }
+          for (int e = 0; e < 32; ++e)
+            y[e] = (__uint_as_float(r[e]) - mu) * inv * __ldg(ea.g + c + e) + __ldg(ea.b + c + e);
+          if (ea.Cf) emit(c / 32, y, true);
+          if (ea.Cs) emit(c / 32, y, false);
         }
       }
+      static_assert(OUT_COLS >= 32 || EPI == TEPI_SWIGLU, "32-column output blocks");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);  // the MMA issuer may reuse this accumulator
     }
-    (void)ok;
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == 5) tmem_dealloc(tmem, C::NACC * C::TMEM_COLS);
 }
 
 // bf16 [n2 x n1 x n0] (n0 innermost, contiguous), box = box1 rows x 64 x 1, SWIZZLE_128B
@@ -318,9 +318,16 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  dim3 grid((unsigned)((M + 127) / 128), (unsigned)(N / BN));
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 1;
+  }
+  const int64_t ntiles = (M + 127) / 128 * (N / BN);
   note_launch();
-  k_tc_gemm<BN, EPI><<<grid, 192, C::SMEM, st>>>(ma, mb, (int)M, N, K, alpha, ea);
+  k_tc_gemm<BN, EPI><<<(unsigned)std::min<int64_t>(ntiles, nsm), 192, C::SMEM, st>>>(ma, mb, (int)M, N, K, alpha, ea);
   return cudaGetLastError();
 }
 
