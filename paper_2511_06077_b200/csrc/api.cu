@@ -902,7 +902,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, (uint8_t *)h->pin.p + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
   if (ctal_bytes)
     CU(cudaMemcpyAsync(h->ctal.p, (uint8_t *)h->pin.p + items_bytes + mi_bytes, ctal_bytes, cudaMemcpyHostToDevice, st));
-  const size_t part_bytes = (size_t)part_rows * stca::part_stride(d) * 4;
+  const size_t part_bytes = (size_t)part_rows * stca::part_row_bytes(d, es);
   if (part_rows) CU(h->part.ensure(part_bytes));
   if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G));
 
@@ -933,7 +933,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
       merged_from = h->partg.as<float>();
     }
     CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, merged_from, d,
-                            G, (int64_t)(part_bytes / 4), h->Y.p, st));
+                            G, (int64_t)part_bytes, h->Y.p, st));
     // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
     s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,
              Zd + (size_t)(i - 1) * d, (int64_t)M * d, Nt, d, hh * d, st);

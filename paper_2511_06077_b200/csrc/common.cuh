@@ -37,8 +37,10 @@ struct AttnItem {
   int32_t pad;
 };
 
-// Split-K partial row layout (fp32): O[0, d) | m (log2 domain) | l | 2 pad -> 16-byte rows
-__host__ __device__ constexpr int part_stride(int d) { return d + 4; }
+// Split-K partial row (one query row of one key chunk), 16-byte aligned:
+//   O^ = O / l, the chunk's normalised output, d elements of the storage type S (bf16 on the bf16
+//   path, exactly what a single-chunk request writes to Y) | m (log2 domain, fp32) | l (fp32) | 8 pad
+__host__ __device__ constexpr int part_row_bytes(int d, int elem_bytes) { return d * elem_bytes + 16; }
 
 // Merge item: one multi-chunk request.
 struct MergeItem {

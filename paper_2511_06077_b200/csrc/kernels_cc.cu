@@ -196,14 +196,12 @@ __global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, c
         if (e < d) Y[(it.qrow0 + q) * d + e] = from_f<S>(O[rr][k] * inv);
       }
     } else {
-      float *pr = part + (it.part_row + q) * (int64_t)part_stride(d);
-      if (lane == 0) {
-        pr[d] = mrow[rr];
-        pr[d + 1] = lrow[rr];
-      }
+      uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + q) * (int64_t)part_row_bytes(d, sizeof(S));
+      const float inv = 1.f / lrow[rr];
+      if (lane == 0) *reinterpret_cast<float2 *>(pr + d * sizeof(S)) = make_float2(mrow[rr], lrow[rr]);
       for (int k = 0; k < nd; ++k) {
         int e = lane + 32 * k;
-        if (e < d) pr[e] = O[rr][k];
+        if (e < d) reinterpret_cast<S *>(pr)[e] = from_f<S>(O[rr][k] * inv);
       }
     }
   }
@@ -227,35 +225,49 @@ cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const Attn
 }
 
 // --------------------------------------------------------------------------
-// split-K LSE merge (K-E): fold chunks 0..C-1 in order, per query row
-//   mu* = max_c mu_c; l* = sum_c 2^(mu_c - mu*) l_c; Y = sum_c 2^(mu_c - mu*) O_c / l*
-// In split-history mode (G > 1) `part` holds every rank's partial buffer (rank-major, stride
-// rank_stride floats) and chunk c of a request with C chunks is read from its owner rank
-// floor(c G / C); with G = 1 this is the intra-GPU split-K merge.
+// split-K LSE merge (K-E): fold chunks 0..C-1 in order, per query row, from the normalised chunk
+// outputs O^_c = O_c / l_c:  mu* = max_c mu_c;  w_c = 2^(mu_c - mu*) l_c;  Y = sum_c w_c O^_c / sum_c w_c
+// (= sum_c 2^(mu_c - mu*) O_c / l*).  In split-history mode (G > 1) `part` holds every rank's
+// partial buffer (rank-major, rank_stride BYTES) and chunk c of a request with C chunks is read from
+// its owner rank floor(c G / C); with G = 1 this is the intra-GPU split-K merge.
 // grid: (items, row blocks of 8 rows), warp per row.
 // --------------------------------------------------------------------------
 template <typename S>
-__global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ items, const float *__restrict__ part,
+__device__ __forceinline__ float4 load4(const uint8_t *p);
+template <>
+__device__ __forceinline__ float4 load4<float>(const uint8_t *p) {
+  return __ldg(reinterpret_cast<const float4 *>(p));
+}
+template <>
+__device__ __forceinline__ float4 load4<bf16>(const uint8_t *p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+  return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u), __uint_as_float(v.y << 16),
+                     __uint_as_float(v.y & 0xffff0000u));
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ items, const uint8_t *__restrict__ part,
                                                 int d, int G, int64_t rank_stride, S *__restrict__ Y) {
   constexpr int MAXC = 8;  // chunks per request handled in registers (C <= 8: L <= 8 x chunk_keys)
   const MergeItem it = items[blockIdx.x];
   const int q = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (q >= it.rows) return;
-  const int64_t stride = (int64_t)it.rows * part_stride(d);
-  const float *p0 = part + (it.part_row + q) * (int64_t)part_stride(d);
+  const int64_t rb = part_row_bytes(d, sizeof(S));
+  const int64_t stride = (int64_t)it.rows * rb;
+  const uint8_t *p0 = part + (it.part_row + q) * rb;
   // chunk c's partial lives in rank floor(c G / C)'s buffer; offsets computed once per row
   int64_t off[MAXC];
   float w[MAXC];
   float2 ml[MAXC];  // (m, l) of every chunk: one 8-byte load each, all issued before any use
-  float4 a0[MAXC];  // and the first 128 O columns of every chunk (no dependence on the weights)
+  float4 a0[MAXC];  // and the first 128 output columns of every chunk (no dependence on the weights)
   float mu = -INFINITY;
   const int e0 = lane * 4;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (c < it.nchunks) {
       off[c] = (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride;
-      ml[c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d));
-      if (e0 < d) a0[c] = __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e0));
+      ml[c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d * sizeof(S)));
+      if (e0 < d) a0[c] = load4<S>(p0 + off[c] + e0 * sizeof(S));
     }
   }
 #pragma unroll
@@ -265,17 +277,17 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (c < it.nchunks) {
-      w[c] = exp2f(ml[c].x - mu);  // fold weight of chunk c (in chunk order below)
-      l += w[c] * ml[c].y;
+      w[c] = exp2f(ml[c].x - mu) * ml[c].y;  // fold weight of chunk c (in chunk order below)
+      l += w[c];
     }
   }
   const float inv = 1.f / l;
-  for (int e = e0; e < d; e += 128) {  // d % 4 == 0: 16-B vector loads of the O rows
+  for (int e = e0; e < d; e += 128) {  // d % 4 == 0: 4 elements per lane per step
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c < it.nchunks) {
-        const float4 a = e == e0 ? a0[c] : __ldg(reinterpret_cast<const float4 *>(p0 + off[c] + e));
+        const float4 a = e == e0 ? a0[c] : load4<S>(p0 + off[c] + e * sizeof(S));
         acc.x += w[c] * a.x;
         acc.y += w[c] * a.y;
         acc.z += w[c] * a.z;
@@ -295,14 +307,14 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
 }
 
 cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
-                           int d, int G, int64_t rank_stride, void *Y, cudaStream_t st) {
+                           int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   dim3 grid((unsigned)n_items, (unsigned)((max_rows + 7) / 8));
   note_launch();
   if (is_bf16)
-    k_merge<bf16><<<grid, 256, 0, st>>>(items, part, d, G, rank_stride, (bf16 *)Y);
+    k_merge<bf16><<<grid, 256, 0, st>>>(items, (const uint8_t *)part, d, G, rank_stride_bytes, (bf16 *)Y);
   else
-    k_merge<float><<<grid, 256, 0, st>>>(items, part, d, G, rank_stride, (float *)Y);
+    k_merge<float><<<grid, 256, 0, st>>>(items, (const uint8_t *)part, d, G, rank_stride_bytes, (float *)Y);
   return cudaGetLastError();
 }
 

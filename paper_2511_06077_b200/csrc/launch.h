@@ -25,7 +25,7 @@ cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float
 cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const AttnItem *items, int64_t n_items, int d,
                          void *Y, float *part, cudaStream_t st);
 cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
-                           int d, int G, int64_t rank_stride, void *Y, cudaStream_t st);
+                           int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st);
 
 // ---- utility kernels ----
 cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg /*[n][3]: src,dst,len*/, int64_t nseg,

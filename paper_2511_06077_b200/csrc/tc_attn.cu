@@ -54,9 +54,8 @@ constexpr int AT_U_BYTES = AT_BM * AT_D * 2;   // 32 KB (two SW128 boxes)
 constexpr int AT_NP = 2;                       // key-column parts per query row (threads per row)
 constexpr int AT_CW = AT_BN / AT_NP;           // key columns (and O columns) per softmax thread
 constexpr int AT_NSW = 4 * AT_NP;              // softmax warps
-constexpr int AT_PSTRIDE = AT_D + 4;           // partial row: O[d] | m | l | pad 2 (16-byte rows)
-constexpr int AT_YSTRIDE = AT_D * 2 + 16;      // staged Y row (bytes, padded: conflict-free)
-constexpr int AT_STAGE_BYTES = AT_BM * AT_PSTRIDE * 4;  // 66 KB epilogue staging; U tile at its start
+constexpr int AT_YSTRIDE = AT_D * 2 + 16;      // staged output row (bytes): Y, or a partial row O/l | m | l | pad
+constexpr int AT_STAGE_BYTES = AT_BM * AT_YSTRIDE;  // 34 KB epilogue staging; the next U tile lands at its start
 constexpr int AT_MAXI = 128;                  // work items of a CTA cached in shared memory
 constexpr int AT_SMEM = 1024 + AT_STAGES * AT_X_BYTES + AT_STAGE_BYTES + AT_MAXI * (int)sizeof(AttnItem) + 256;
 constexpr float AT_RESCALE_THRESHOLD = 8.f;    // log2(256)
@@ -350,29 +349,21 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const bool single = it.part_row < 0;
       const float inv = 1.f / lrow;
 #pragma unroll 1
-      for (int cb = 0; cb < AT_CW; cb += 32) {
+      for (int cb = 0; cb < AT_CW; cb += 32) {  // Y row, or the partial's normalised O / l (same bf16 form)
         uint32_t o[32];
         tmem_ld16x2_32<64>(tmem + lane_off + AT_TO + cb, o);
         tmem_ld_wait();
-        if (single) {
-          uint8_t *dst = sStage + row * AT_YSTRIDE + (AT_CW * pp + cb) * 2;
+        uint8_t *dst = sStage + row * AT_YSTRIDE + (AT_CW * pp + cb) * 2;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            *reinterpret_cast<uint4 *>(dst + 16 * i) =
-                make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
-                           pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
-                           pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
-                           pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
-        } else {
-          float *dst = reinterpret_cast<float *>(sStage) + row * AT_PSTRIDE + AT_CW * pp + cb;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            *reinterpret_cast<uint4 *>(dst + 4 * i) = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-        }
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint4 *>(dst + 16 * i) =
+              make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                         pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                         pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                         pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
       }
       if (!single && pp == 0)
-        *reinterpret_cast<float4 *>(reinterpret_cast<float *>(sStage) + row * AT_PSTRIDE + AT_D) =
-            make_float4(m, lrow, 0.f, 0.f);
+        *reinterpret_cast<float4 *>(sStage + row * AT_YSTRIDE + AT_D * 2) = make_float4(m, lrow, 0.f, 0.f);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);  // PV of the next item may overwrite O
@@ -387,8 +378,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         if (single) {  // one 256-byte row per copy (the staging rows are padded)
           for (int r = lane; r < it.nq; r += 32)
             bulk_store(Y + (it.qrow0 + r) * AT_D, sStage + r * AT_YSTRIDE, AT_D * 2);
-        } else if (lane == 0) {
-          bulk_store(part + it.part_row * AT_PSTRIDE, sStage, (uint32_t)it.nq * AT_PSTRIDE * 4);
+        } else if (lane == 0) {  // partial rows are contiguous with the staging's row stride
+          bulk_store(reinterpret_cast<uint8_t *>(part) + it.part_row * AT_YSTRIDE, sStage, (uint32_t)it.nq * AT_YSTRIDE);
         }
         bulk_commit();
         bulk_pending = true;

@@ -252,14 +252,17 @@ __global__ void __launch_bounds__(352, 1)
                                 pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
                                 pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
         } else {
-          float *pr = part + (it.part_row + r) * (int64_t)part_stride(D);
-          if (col == 0) {
-            pr[D] = sMax[r] > sMax[64 + r] ? sMax[r] : sMax[64 + r];
-            pr[D + 1] = l;
-          }
+          uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + r) * (int64_t)part_row_bytes(D, 2);
+          if (col == 0)
+            *reinterpret_cast<float2 *>(pr + 2 * D) = make_float2(sMax[r] > sMax[64 + r] ? sMax[r] : sMax[64 + r], l);
+          const float inv = 1.f / l;  // partials hold the chunk's normalised output O / l
+          uint4 *dst = reinterpret_cast<uint4 *>(pr + 2 * col);
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<uint4 *>(pr + col + i) = make_uint4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
         }
       }
     }
