@@ -846,7 +846,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   std::vector<int64_t> part_base(B, -1);
   std::vector<stca::MergeItem> mi;
   int64_t part_rows = 0;
-  int max_rows = 0;
+  int max_rows = 0, max_chunks = 0;
   const int G = h->cfg.split_world, grank = h->cfg.split_rank;
   for (int64_t b = 0; b < B; ++b) {
     const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
@@ -856,6 +856,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     mi.push_back({tgt_off[b] * hh, part_rows, (int32_t)rows, nc});
     part_rows += rows * nc;
     max_rows = std::max<int>(max_rows, (int)rows);
+    max_chunks = std::max<int>(max_chunks, (int)nc);
   }
   std::vector<stca::AttnItem> items;
   items.reserve((size_t)nit);
@@ -932,7 +933,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
         return fail(h, STCA_ERR_COMM, "split-history exchange failed at layer %d", i);
       merged_from = h->partg.as<float>();
     }
-    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, merged_from, d,
+    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
                             G, (int64_t)part_bytes, h->Y.p, st));
     // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
     s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,

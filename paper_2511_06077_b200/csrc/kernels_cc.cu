@@ -245,76 +245,94 @@ __device__ __forceinline__ float4 load4<bf16>(const uint8_t *p) {
                      __uint_as_float(v.y & 0xffff0000u));
 }
 
-template <typename S>
+template <typename S, int MAXC, int RPW>
 __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ items, const uint8_t *__restrict__ part,
                                                 int d, int G, int64_t rank_stride, S *__restrict__ Y) {
-  constexpr int MAXC = 8;  // chunks per request handled in registers (C <= 8: L <= 8 x chunk_keys)
+  // MAXC: chunks per request handled in registers (C <= MAXC); RPW: rows per warp, all of their
+  // loads issued before any use (the merge is latency-bound: more bytes in flight per thread)
   const MergeItem it = items[blockIdx.x];
-  const int q = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (q >= it.rows) return;
+  const int lane = threadIdx.x % 32;
+  const int qw = (blockIdx.y * 8 + threadIdx.x / 32) * RPW;  // this warp's first row
+  if (qw >= it.rows) return;
   const int64_t rb = part_row_bytes(d, sizeof(S));
   const int64_t stride = (int64_t)it.rows * rb;
-  const uint8_t *p0 = part + (it.part_row + q) * rb;
-  // chunk c's partial lives in rank floor(c G / C)'s buffer; offsets computed once per row
-  int64_t off[MAXC];
-  float w[MAXC];
-  float2 ml[MAXC];  // (m, l) of every chunk: one 8-byte load each, all issued before any use
-  float4 a0[MAXC];  // and the first 128 output columns of every chunk (no dependence on the weights)
-  float mu = -INFINITY;
+  int64_t off[MAXC];  // chunk c's partial lives in rank floor(c G / C)'s buffer
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) off[c] = c < it.nchunks ? (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride : 0;
   const int e0 = lane * 4;
+  float2 ml[RPW][MAXC];  // (m, l) of every row and chunk
+  float4 a0[RPW][MAXC];  // and the first 128 output columns
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    if (c < it.nchunks) {
-      off[c] = (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride;
-      ml[c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d * sizeof(S)));
-      if (e0 < d) a0[c] = load4<S>(p0 + off[c] + e0 * sizeof(S));
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c)
-    if (c < it.nchunks) mu = fmaxf(mu, ml[c].x);
-  float l = 0.f;
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    if (c < it.nchunks) {
-      w[c] = exp2f(ml[c].x - mu) * ml[c].y;  // fold weight of chunk c (in chunk order below)
-      l += w[c];
-    }
-  }
-  const float inv = 1.f / l;
-  for (int e = e0; e < d; e += 128) {  // d % 4 == 0: 4 elements per lane per step
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < RPW; ++r) {
+    const uint8_t *p0 = part + (it.part_row + qw + r) * rb;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
-      if (c < it.nchunks) {
-        const float4 a = e == e0 ? a0[c] : load4<S>(p0 + off[c] + e * sizeof(S));
-        acc.x += w[c] * a.x;
-        acc.y += w[c] * a.y;
-        acc.z += w[c] * a.z;
-        acc.w += w[c] * a.w;
+      if (qw + r < it.rows && c < it.nchunks) {
+        ml[r][c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d * sizeof(S)));
+        if (e0 < d) a0[r][c] = load4<S>(p0 + off[c] + e0 * sizeof(S));
       }
     }
-    S *yr = Y + (it.qrow0 + q) * d + e;
-    if constexpr (sizeof(S) == 2) {  // four bf16 in one 8-byte store
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-      *reinterpret_cast<uint2 *>(yr) = make_uint2(*reinterpret_cast<const uint32_t *>(&lo),
-                                                  *reinterpret_cast<const uint32_t *>(&hi));
-    } else {
-      *reinterpret_cast<float4 *>(yr) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int q = qw + r;
+    if (q >= it.rows) break;
+    const uint8_t *p0 = part + (it.part_row + q) * rb;
+    float mu = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < it.nchunks) mu = fmaxf(mu, ml[r][c].x);
+    float w[MAXC], l = 0.f;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      w[c] = 0.f;
+      if (c < it.nchunks) {
+        w[c] = exp2f(ml[r][c].x - mu) * ml[r][c].y;  // fold weight of chunk c (in chunk order below)
+        l += w[c];
+      }
+    }
+    const float inv = 1.f / l;
+    for (int e = e0; e < d; e += 128) {  // d % 4 == 0: 4 elements per lane per step
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        if (c < it.nchunks) {
+          const float4 a = e == e0 ? a0[r][c] : load4<S>(p0 + off[c] + e * sizeof(S));
+          acc.x += w[c] * a.x;
+          acc.y += w[c] * a.y;
+          acc.z += w[c] * a.z;
+          acc.w += w[c] * a.w;
+        }
+      }
+      S *yr = Y + (it.qrow0 + q) * d + e;
+      if constexpr (sizeof(S) == 2) {  // four bf16 in one 8-byte store
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+        *reinterpret_cast<uint2 *>(yr) = make_uint2(*reinterpret_cast<const uint32_t *>(&lo),
+                                                    *reinterpret_cast<const uint32_t *>(&hi));
+      } else {
+        *reinterpret_cast<float4 *>(yr) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      }
     }
   }
 }
 
-cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
-                           int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st) {
+cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, int max_chunks,
+                           const float *part, int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
-  dim3 grid((unsigned)n_items, (unsigned)((max_rows + 7) / 8));
+  const uint8_t *p = (const uint8_t *)part;
   note_launch();
-  if (is_bf16)
-    k_merge<bf16><<<grid, 256, 0, st>>>(items, (const uint8_t *)part, d, G, rank_stride_bytes, (bf16 *)Y);
-  else
-    k_merge<float><<<grid, 256, 0, st>>>(items, (const uint8_t *)part, d, G, rank_stride_bytes, (float *)Y);
+#define STCA_MERGE(S, MC, RPW)                                                                              \
+  k_merge<S, MC, RPW><<<dim3((unsigned)n_items, (unsigned)((max_rows + 8 * RPW - 1) / (8 * RPW))), 256, 0, st>>>( \
+      items, p, d, G, rank_stride_bytes, (S *)Y)
+  if (max_chunks <= 2) {  // the common case (a 10k history at the default cap): 4 rows per warp
+    if (is_bf16) STCA_MERGE(bf16, 2, 4);
+    else STCA_MERGE(float, 2, 4);
+  } else {
+    if (is_bf16) STCA_MERGE(bf16, 8, 1);
+    else STCA_MERGE(float, 8, 1);
+  }
+#undef STCA_MERGE
   return cudaGetLastError();
 }
 

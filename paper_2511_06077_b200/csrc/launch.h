@@ -24,7 +24,8 @@ cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float
 // online-softmax sweep over items (qtile <= 16 rows per item)
 cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const AttnItem *items, int64_t n_items, int d,
                          void *Y, float *part, cudaStream_t st);
-cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, const float *part,
+cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, int max_chunks,
+                           const float *part,
                            int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st);
 
 // ---- utility kernels ----
