@@ -86,14 +86,13 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// two gates at once with packed fp32x2 arithmetic (FMUL2 / FFMA2): half the FMA-pipe instructions
+// two gates at once with packed fp32x2 arithmetic (FMUL2 / FFMA2): half the FMA-pipe instructions.
+// u v sigmoid(v) = a + a tanh(v/2) with a = u (v/2): two MUFU ops and three packed FMA-pipe ops.
 __device__ __forceinline__ uint32_t swiglu2(float u0, float v0, float u1, float v1) {
-  const uint64_t v2 = f2_pack(v0, v1), half2 = f2_pack(0.5f, 0.5f);
-  const uint64_t hv = f2_mul(v2, half2);
+  const uint64_t hv = f2_mul(f2_pack(v0, v1), f2_pack(0.5f, 0.5f));  // v / 2
   const uint64_t t2 = f2_pack(tanh_approx(f2_lo(hv)), tanh_approx(f2_hi(hv)));
-  const uint64_t sg = f2_fma(t2, half2, half2);           // sigmoid(v) = 0.5 tanh(v/2) + 0.5
-  const uint64_t uv = f2_mul(f2_pack(u0, u1), v2);
-  const uint64_t h2 = f2_mul(uv, sg);
+  const uint64_t a2 = f2_mul(f2_pack(u0, u1), hv);                   // u v / 2
+  const uint64_t h2 = f2_fma(a2, t2, a2);
   return pack_bf16(f2_lo(h2), f2_hi(h2));
 }
 
