@@ -87,3 +87,31 @@ def test_target_permutation_permutes_outputs_bit_exact():
                             tgt_off=wl.tgt_off, X=wl.X, xt=wl.xt[perm], X_bits=wl.X_bits, xt_bits=wl.xt_bits[perm])
     Zp, zp = run_gpu(wl2)
     assert np.array_equal(Zp, Z[perm]) and np.array_equal(zp, z[perm])
+
+
+def test_degenerate_batches():
+    """No targets at all (every m_b = 0): forward is a no-op on zero rows; a batch whose requests all
+    have one history row and one target; repeated forwards on one projection are bit-identical."""
+    import torch
+    import paper_2511_06077_b200 as stca
+    cfg = make_cfg(B=3, m=1, M=2)
+    wl = workload.make_workload(cfg, seed=21, lengths=np.array([5, 1, 300]))
+    c = wl.cfg
+    m = stca.STCA(workload.full_weights(wl), d=c.d, h=c.h, r=c.r, M=c.M)
+    X, xt = device_inputs(wl)
+    m.project_history(X, wl.hist_off)
+    Z0 = torch.zeros(0, c.M, c.d, device="cuda")
+    m.forward(xt[:0], np.zeros(4, dtype=np.int64), Z0, torch.zeros(0, c.d, device="cuda"))
+    torch.cuda.synchronize()
+    Z1 = torch.full((wl.Nt, c.M, c.d), float("nan"), device="cuda")
+    Z2 = torch.full((wl.Nt, c.M, c.d), float("nan"), device="cuda")
+    m.forward(xt, wl.tgt_off, Z1)
+    m.forward(xt, wl.tgt_off, Z2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(Z1).all() and torch.equal(Z1, Z2)
+    Zr, _, rows = oracle.forward_workload(wl, nthreads=2)
+    assert rowrel(Z1.cpu().numpy()[rows], Zr).max() <= 2e-2
+    wl1 = workload.make_workload(make_cfg(B=4, m=1, M=2), seed=22, lengths=np.ones(4, dtype=np.int64))
+    Z, z = run_gpu(wl1)
+    Zr, zr, rows = oracle.forward_workload(wl1, nthreads=2)
+    assert rowrel(Z[rows], Zr).max() <= 2e-2 and rowrel(z[rows], zr).max() <= 2e-2
