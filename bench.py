@@ -189,6 +189,8 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+            os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line (NCCL prints its version otherwise)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # split1 (BASELINE config 5): ONE L = 10k history split over the ranks (split-history, strong
     # scaling, one all-gather of partials per layer); every other config: each rank its own shard
