@@ -26,6 +26,11 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// programmatic dependent launch (launch_pdl): wait for the predecessor grid's results / let the
+// successor grid be scheduled
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Device-side attention work item (host plan -> device), 48 bytes.
 struct AttnItem {
   int64_t qrow0;     // first query row (row index into U / Y, = target*h + head)

@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
                                                 int d, int G, int64_t rank_stride, S *__restrict__ Y) {
   // MAXC: chunks per request handled in registers (C <= MAXC); RPW: rows per warp, all of their
   // loads issued before any use (the merge is latency-bound: more bytes in flight per thread)
+  pdl_wait();  // the attention's partials are complete and visible
+  pdl_trigger();
   const MergeItem it = items[blockIdx.x];
   const int lane = threadIdx.x % 32;
   const int qw = (blockIdx.y * 8 + threadIdx.x / 32) * RPW;  // this warp's first row
@@ -322,9 +324,12 @@ cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items
   if (n_items <= 0) return cudaSuccess;
   const uint8_t *p = (const uint8_t *)part;
   note_launch();
-#define STCA_MERGE(S, MC, RPW)                                                                              \
-  k_merge<S, MC, RPW><<<dim3((unsigned)n_items, (unsigned)((max_rows + 8 * RPW - 1) / (8 * RPW))), 256, 0, st>>>( \
-      items, p, d, G, rank_stride_bytes, (S *)Y)
+#define STCA_MERGE(S, MC, RPW)                                                                                    \
+  do {                                                                                                           \
+    cudaError_t e = launch_pdl(k_merge<S, MC, RPW>, dim3((unsigned)n_items, (unsigned)((max_rows + 8 * RPW - 1) / (8 * RPW))), \
+                               dim3(256), 0, st, items, p, d, G, rank_stride_bytes, (S *)Y);                       \
+    if (e != cudaSuccess) return e;                                                                              \
+  } while (0)
   if (max_chunks <= 2) {  // the common case (a 10k history at the default cap): 4 rows per warp
     if (is_bf16) STCA_MERGE(bf16, 2, 4);
     else STCA_MERGE(float, 2, 4);

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace stca {
@@ -11,6 +13,27 @@ enum Epi { EPI_STORE = 0, EPI_SWIGLU = 1 };
 
 // process-wide count of kernels launched by libstca (stca_kernel_launches())
 void note_launch(int n = 1);
+
+// Programmatic dependent launch for the forward's kernel chain: the kernel may be scheduled while
+// its predecessor in the stream drains, so its launch and prologue (barrier init, TMEM alloc,
+// tensor-map prefetch) overlap the predecessor's tail.  Every kernel launched this way executes
+// griddepcontrol.wait (pdl_wait) before its first global-memory access, and signals its own
+// dependents (pdl_trigger) right after its prologue.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- CUDA-core kernels (fp32 path; reference-grade, K-G of SURVEY §2.2) ----
 // C = alpha * A[MxK] B[KxN]; A, B row-major storage S (lda, ldb);

@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == AT_WS) tmem_alloc(tslot, 512);
+  pdl_wait();     // the predecessor's outputs (U) are complete and visible
+  pdl_trigger();
   for (int k = threadIdx.x; k < ni && k < AT_MAXI; k += blockDim.x) sItem[k] = items[cta_items[i0 + k]];
   tc_fence_before();
   __syncthreads();
@@ -428,8 +430,9 @@ cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, 
   const char *trace_path = getenv("STCA_TRACE_ATTN");  // debug only: clock64 stamps of CTA 0
   if (trace_path && cudaMalloc(&trace, 8192 * 8) == cudaSuccess) cudaMemsetAsync(trace, 0, 8192 * 8, st);
   note_launch();
-  tc::k_tc_attention<<<(unsigned)n_ctas, tc::AT_THREADS, tc::AT_SMEM, st>>>(mx, mu, items, cta_off, cta_items,
-                                                                              (bf16 *)Y, part, trace);
+  cudaError_t e = launch_pdl(tc::k_tc_attention, dim3((unsigned)n_ctas), dim3(tc::AT_THREADS), tc::AT_SMEM, st, mx, mu,
+                             items, cta_off, cta_items, (bf16 *)Y, part, trace);
+  if (e != cudaSuccess) return e;
   if (trace) {
     static unsigned long long h[8192];
     cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);

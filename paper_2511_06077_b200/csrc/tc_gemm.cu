@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();     // the predecessor's outputs (our A) are complete and visible
+  pdl_trigger();  // the successor may be scheduled (it waits for us the same way)
 
   if (warp == 4) {
     if (lane == 0) {  // TMA producer
@@ -327,8 +329,9 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
   }
   const int64_t ntiles = (M + 127) / 128 * (N / BN);
   note_launch();
-  k_tc_gemm<BN, EPI><<<(unsigned)std::min<int64_t>(ntiles, nsm), 192, C::SMEM, st>>>(ma, mb, (int)M, N, K, alpha, ea);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(k_tc_gemm<BN, EPI>, dim3((unsigned)std::min<int64_t>(ntiles, nsm)), dim3(192), C::SMEM, st,
+                             ma, mb, (int)M, N, K, alpha, ea);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace tc
