@@ -78,15 +78,19 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tiles_m = (M + C::BM - 1) / C::BM, ntiles = tiles_m * (N / BN);
+  // 2-CTA clusters: the two CTAs take the two m-tiles of a tile pair with the same n-tile, and each
+  // fetches half of every B (weight) slot for BOTH by TMA multicast, so B leaves L2 once per pair
+  // (B dominates the traffic: N is the full output width, and every m-tile re-reads all of it)
+  const int tiles_m = (M + C::BM - 1) / C::BM, pm = (tiles_m + 1) / 2, npairs = pm * (N / BN);
   const int nk = (K + C::BK - 1) / C::BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (warp == 4 && lane == 0) {
     tma_prefetch(&mapA);
     tma_prefetch(&mapB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);  // both CTAs' MMAs have read the slot (the peer multicasts into it)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
@@ -96,25 +100,27 @@ __global__ void __launch_bounds__(192, 1)
   }
   if (warp == 5) tmem_alloc(tslot, C::NACC * C::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barrier inits visible cluster-wide before the peer multicasts into this CTA
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  const uint32_t crank = cluster_ctarank();
   pdl_wait();     // the predecessor's outputs (our A) are complete and visible
   pdl_trigger();  // the successor may be scheduled (it waits for us the same way)
 
   if (warp == 4) {
     if (lane == 0) {  // TMA producer
       int s = 0, ph = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t % tiles_m) * C::BM, n0 = (t / tiles_m) * BN;
+      for (int p = cid; p < npairs; p += ncl) {
+        const int m0 = (2 * (p % pm) + (int)crank) * C::BM, n0 = (p / pm) * BN;  // m0 >= M: TMA zero-fills
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t *sa = smem + s * C::STAGE, *sb = sa + C::A_BYTES;
-          mbar_expect_tx(&full[s], C::STAGE);
+          mbar_expect_tx(&full[s], C::STAGE);  // own A + both B halves
           tma_load_2d(sa, &mapA, &full[s], kb * C::BK, m0);
 #pragma unroll
-          for (int j = 0; j < BN / C::NS; ++j)
-            tma_load_2d(sb + j * C::NS * 128, &mapB, &full[s], kb * C::BK, n0 + j * C::NS);
+          for (int j = 0; j < BN / C::NS; ++j)  // this CTA's half of each NS-row block, to both CTAs
+            tma_load_2d_mc(sb + (j * C::NS + (int)crank * (C::NS / 2)) * 128, &mapB, &full[s], kb * C::BK,
+                           n0 + j * C::NS + (int)crank * (C::NS / 2), 0x3, policy_evict_last());
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = idesc_bf16(128, C::NS, 0);
       int s = 0, ph = 0, i = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      for (int p = cid; p < npairs; p += ncl, ++i) {
         const int a = i % C::NACC;
         mbar_wait(&acc_empty[a], ((i / C::NACC) & 1) ^ 1);  // the epilogue has read this accumulator
         tc_fence_after();
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(192, 1)
               umma_f16_ss(acc + j * C::NS, ad, bd, idesc, (kb | k) != 0);
             }
           }
-          umma_commit(&empty[s]);
+          umma_commit_mc(&empty[s], 0x3);  // the slot is free again in both CTAs
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&acc_full[a]);
@@ -155,8 +161,8 @@ __global__ void __launch_bounds__(192, 1)
     const int row = q * 32 + lane;
     constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
     int i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const int m0 = (t % tiles_m) * C::BM, n0 = (t / tiles_m) * BN;
+    for (int p = cid; p < npairs; p += ncl, ++i) {
+      const int m0 = (2 * (p % pm) + (int)crank) * C::BM, n0 = (p / pm) * BN;
       const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
       const int a = i % C::NACC;
       mbar_wait(&acc_full[a], (i / C::NACC) & 1);
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // the peer no longer multicasts into / arrives on this CTA
   if (warp == 5) tmem_dealloc(tmem, C::NACC * C::TMEM_COLS);
 }
 
@@ -313,24 +319,51 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
                                const EpiArgs &ea, cudaStream_t st) {
   using C = GemmCfg<BN>;
   CUtensorMap ma, mb;
-  if (!make_map_bf16(&ma, A, M, K, lda, 128) || !make_map_bf16(&mb, Bt, N, K, K, C::NS)) return cudaErrorInvalidValue;
+  if (!make_map_bf16(&ma, A, M, K, lda, 128) || !make_map_bf16(&mb, Bt, N, K, K, C::NS / 2)) return cudaErrorInvalidValue;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 1;
+  static int mc = 0;  // co-resident 2-CTA clusters of this instantiation
+  if (!mc) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cudaLaunchAttribute ca[1];
+    ca[0].id = cudaLaunchAttributeClusterDimension;
+    ca[0].val.clusterDim.x = 2;
+    ca[0].val.clusterDim.y = 1;
+    ca[0].val.clusterDim.z = 1;
+    cfg.attrs = ca;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&mc, (const void *)k_tc_gemm<BN, EPI>, &cfg) != cudaSuccess || mc <= 0) {
+      cudaGetLastError();
+      int dev = 0, nsm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      mc = nsm > 1 ? nsm / 2 : 1;
+    }
   }
-  const int64_t ntiles = (M + 127) / 128 * (N / BN);
+  const int64_t npairs = ((M + 127) / 128 + 1) / 2 * (N / BN);
   note_launch();
-  cudaError_t e = launch_pdl(k_tc_gemm<BN, EPI>, dim3((unsigned)std::min<int64_t>(ntiles, nsm)), dim3(192), C::SMEM, st,
-                             ma, mb, (int)M, N, K, alpha, ea);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(npairs, mc)));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (launch.h)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tc_gemm<BN, EPI>, ma, mb, (int)M, N, K, alpha, ea);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
