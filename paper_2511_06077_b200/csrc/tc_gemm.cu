@@ -3,7 +3,8 @@
 //   C[M x N] = A[M x K] . Bt^T,   A bf16 row-major (lda), Bt = B^T bf16 [N x K] (K-major)
 //
 // Warps 0-3: epilogue; warp 4: TMA producer (SWIZZLE_128B boxes of 64 K-elements); warp 5: TMEM
-// allocator + single-thread tcgen05.mma issuer (M = 128, N-slices <= 256, K = 16 per instruction;
+// allocator + single-thread tcgen05.mma issuer of the CTA pair (cta_group::2: M = 256 over the two
+// CTAs of a cluster, N-slices <= 256, K = 16 per instruction;
 // highest warp ids so the arbiter never starves the issuing thread).  Epilogue: one thread per accumulator row (TMEM lane), reading the fp32
 // accumulator with tcgen05.ld.  Epilogues:
 //   TEPI_STORE  : alpha*acc -> bf16 (Cs) and/or fp32 (Cf)
@@ -45,20 +46,21 @@ __device__ __forceinline__ float silu_f(float v) {  // v * sigmoid(v)
 template <int BN>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int NS = BN < 256 ? BN : 256;  // N per MMA instruction
-  static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int NS = BN < 256 ? BN : 256;  // N per (M = 256, CTA pair) MMA instruction
+  static constexpr int A_BYTES = BM * BK * 2;     // 16 KB: this CTA's 128 rows of A
+  static constexpr int B_BYTES = BN / 2 * BK * 2;  // this CTA's half of every NS-row block of B^T
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int F_STRIDE = 32 * 4 + 16;    // staged fp32 row of a 32-column output block (bytes)
   static constexpr int H_STRIDE = 32 * 2 + 16;    // staged bf16 row
   static constexpr int STG_BYTES = 128 * F_STRIDE;  // one staged output block (dedicated: the ring keeps running)
-  static constexpr int STAGES = (196 * 1024 / STAGE) > 4 ? 4 : (196 * 1024 / STAGE);
+  static constexpr int STAGES = (200 * 1024 / STAGE) > 6 ? 6 : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
   static constexpr int NACC = TMEM_COLS <= 256 ? 2 : 1;  // TMEM accumulators (double-buffered when they fit)
   static constexpr int SMEM = STAGES * STAGE + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// PERSISTENT: grid = min(tiles, SMs); CTA c takes output tiles c, c + grid, ... (m fastest).  The
+// PERSISTENT: grid = 2 x min(tile pairs, co-resident clusters); cluster c takes 256-row tile pairs
+// c, c + clusters, ... (n fastest).  The
 // smem ring runs across tiles and the TMEM accumulator is double-buffered, so the epilogue of tile
 // i (TMEM -> registers -> padded smem block -> coalesced 16-byte stores) overlaps the MMAs of tile
 // i+1 and the loads of tile i+2; per-tile launch / prologue / pipeline-fill costs are paid once
@@ -74,14 +76,18 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(stg + C::STG_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *acc_full = empty + C::STAGES;   // NACC (MMA commit: accumulator a complete)
-  uint64_t *acc_empty = acc_full + 2;       // NACC (4 epilogue warps: accumulator a read)
+  uint64_t *acc_empty = acc_full + 2;       // NACC, leader only (8 epilogue warps of the pair: accumulator a read)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // 2-CTA clusters: the two CTAs take the two m-tiles of a tile pair with the same n-tile, and each
-  // fetches half of every B (weight) slot for BOTH by TMA multicast, so B leaves L2 once per pair
-  // (B dominates the traffic: N is the full output width, and every m-tile re-reads all of it)
-  const int tiles_m = (M + C::BM - 1) / C::BM, pm = (tiles_m + 1) / 2, npairs = pm * (N / BN);
+  // CTA pairs (cta_group::2): a pair computes a 256 x BN tile with M = 256 MMAs issued by the leader
+  // (rank 0); CTA r holds A rows [128 r, 128 r + 128) and half of every NS-row block of B^T, so each
+  // SM receives 16 KB of A + BN/2 x 64 x 2 bytes of B per 64-deep k-block instead of the whole B —
+  // per-SM operand ingest, not L2, is what limits M = 128 tiles at BN >= 256 (a 2-CTA TMA multicast
+  // of B measured within 2%: every SM still receives all of B).
+    // Tile pairs are numbered n-fastest: the pairs in flight share a few 256-row blocks of A (read
+  // from HBM once) and sweep all of B (the weights, L2-resident).
+  const int tiles_m = (M + C::BM - 1) / C::BM, tn = N / BN, npairs = (tiles_m + 1) / 2 * tn;
   const int nk = (K + C::BK - 1) / C::BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -90,15 +96,15 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&mapB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);  // both CTAs' MMAs have read the slot (the peer multicasts into it)
+      mbar_init(&empty[s], 1);  // the leader's MMAs have read the slot (commit multicast to both CTAs)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);
+      mbar_init(&acc_empty[a], 8);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tslot, C::NACC * C::TMEM_COLS);
+  if (warp == 5) tmem_alloc_pair(tslot, C::NACC * C::TMEM_COLS);
   tc_fence_before();
   cluster_sync_all();  // barrier inits visible cluster-wide before the peer multicasts into this CTA
   tc_fence_after();
@@ -111,23 +117,24 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // TMA producer
       int s = 0, ph = 0;
       for (int p = cid; p < npairs; p += ncl) {
-        const int m0 = (2 * (p % pm) + (int)crank) * C::BM, n0 = (p / pm) * BN;  // m0 >= M: TMA zero-fills
+        const int m0 = (2 * (p / tn) + (int)crank) * C::BM, n0 = (p % tn) * BN;  // m0 >= M: TMA zero-fills
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t *sa = smem + s * C::STAGE, *sb = sa + C::A_BYTES;
-          mbar_expect_tx(&full[s], C::STAGE);  // own A + both B halves
-          tma_load_2d(sa, &mapA, &full[s], kb * C::BK, m0);
+          const uint32_t fb = mapa_shared(&full[s], 0);  // both CTAs' bytes complete on the leader's barrier
+          if (crank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE);
+          tma_load_2d_pair(sa, &mapA, fb, kb * C::BK, m0, policy_evict_normal());
 #pragma unroll
-          for (int j = 0; j < BN / C::NS; ++j)  // this CTA's half of each NS-row block, to both CTAs
-            tma_load_2d_mc(sb + (j * C::NS + (int)crank * (C::NS / 2)) * 128, &mapB, &full[s], kb * C::BK,
-                           n0 + j * C::NS + (int)crank * (C::NS / 2), 0x3, policy_evict_last());
+          for (int j = 0; j < BN / C::NS; ++j)  // this CTA's half of each NS-row block of B^T
+            tma_load_2d_pair(sb + j * (C::NS / 2) * 128, &mapB, fb, kb * C::BK,
+                             n0 + j * C::NS + (int)crank * (C::NS / 2), policy_evict_last());
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {  // MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(128, C::NS, 0);
+    if (lane == 0 && crank == 0) {  // MMA issuer (the pair's leader)
+      constexpr uint32_t idesc = idesc_bf16(256, C::NS, 0);
       int s = 0, ph = 0, i = 0;
       for (int p = cid; p < npairs; p += ncl, ++i) {
         const int a = i % C::NACC;
@@ -143,14 +150,14 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
 #pragma unroll
             for (int j = 0; j < BN / C::NS; ++j) {
-              const uint64_t bd = sdesc_sw128(sb + j * C::NS * 128 + k * 32, 16, 1024);
-              umma_f16_ss(acc + j * C::NS, ad, bd, idesc, (kb | k) != 0);
+              const uint64_t bd = sdesc_sw128(sb + j * (C::NS / 2) * 128 + k * 32, 16, 1024);
+              umma_f16_ss_pair(acc + j * C::NS, ad, bd, idesc, (kb | k) != 0);
             }
           }
-          umma_commit_mc(&empty[s], 0x3);  // the slot is free again in both CTAs
+          umma_commit_pair_mc(&empty[s], 0x3);  // the slot is free again in both CTAs
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
-        umma_commit(&acc_full[a]);
+        umma_commit_pair_mc(&acc_full[a], 0x3);  // both CTAs' accumulator halves are complete
       }
     }
   } else {  // epilogue warps 0..3: TMEM lane quarter = warp
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(192, 1)
     constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
     int i = 0;
     for (int p = cid; p < npairs; p += ncl, ++i) {
-      const int m0 = (2 * (p % pm) + (int)crank) * C::BM, n0 = (p / pm) * BN;
+      const int m0 = (2 * (p / tn) + (int)crank) * C::BM, n0 = (p % tn) * BN;
       const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
       const int a = i % C::NACC;
       mbar_wait(&acc_full[a], (i / C::NACC) & 1);
@@ -259,12 +266,12 @@ __global__ void __launch_bounds__(192, 1)
       static_assert(OUT_COLS >= 32 || EPI == TEPI_SWIGLU, "32-column output blocks");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[a]);  // the MMA issuer may reuse this accumulator
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(&acc_empty[a], 0));  // the leader may reuse accumulator a
     }
   }
   tc_fence_before();
   cluster_sync_all();  // the peer no longer multicasts into / arrives on this CTA
-  if (warp == 5) tmem_dealloc(tmem, C::NACC * C::TMEM_COLS);
+  if (warp == 5) tmem_dealloc_pair(tmem, C::NACC * C::TMEM_COLS);
 }
 
 // bf16 [n2 x n1 x n0] (n0 innermost, contiguous), box = box1 rows x 64 x 1, SWIZZLE_128B
