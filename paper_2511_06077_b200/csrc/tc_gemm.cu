@@ -39,8 +39,12 @@ struct EpiArgs {
   float eps;
 };
 
-__device__ __forceinline__ float silu_f(float v) {  // v * sigmoid(v)
-  return __fdividef(v, 1.f + exp2f(-1.4426950408889634f * v));
+// u * silu(v) = u v sigmoid(v) = a + a tanh(v / 2) with a = u v / 2: one MUFU op per output
+__device__ __forceinline__ float swiglu_f(float u, float v) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
+  const float a = 0.5f * u * v;
+  return fmaf(a, t, a);
 }
 
 template <int BN>
@@ -56,7 +60,8 @@ struct GemmCfg {
   static constexpr int STAGES = (200 * 1024 / STAGE) > 6 ? 6 : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
   static constexpr int NACC = TMEM_COLS <= 256 ? 2 : 1;  // TMEM accumulators (double-buffered when they fit)
-  static constexpr int SMEM = STAGES * STAGE + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int LNP_BYTES = 2 * BN * 4;     // LayerNorm gamma | beta, staged once per CTA
+  static constexpr int SMEM = STAGES * STAGE + STG_BYTES + LNP_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // PERSISTENT: grid = 2 x min(tile pairs, co-resident clusters); cluster c takes 256-row tile pairs
@@ -73,7 +78,8 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *stg = smem + C::STAGES * C::STAGE;
-  uint64_t *full = reinterpret_cast<uint64_t *>(stg + C::STG_BYTES);
+  float *lnp = reinterpret_cast<float *>(stg + C::STG_BYTES);  // LN: gamma [BN] | beta [BN]
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + C::STG_BYTES + C::LNP_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *acc_full = empty + C::STAGES;   // NACC (MMA commit: accumulator a complete)
   uint64_t *acc_empty = acc_full + 2;       // NACC, leader only (8 epilogue warps of the pair: accumulator a read)
@@ -167,6 +173,13 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
+    if (EPI == TEPI_LN) {  // gamma/beta from SMEM: global loads in flight stall this warp's tcgen05.ld
+      for (int c = threadIdx.x; c < BN; c += 128) {
+        lnp[c] = ea.g[c];
+        lnp[BN + c] = ea.b[c];
+      }
+      named_bar_sync(1, 128);
+    }
     int i = 0;
     for (int p = cid; p < npairs; p += ncl, ++i) {
       const int m0 = (2 * (p / tn) + (int)crank) * C::BM, n0 = (p % tn) * BN;
@@ -202,65 +215,82 @@ __global__ void __launch_bounds__(192, 1)
         }
         named_bar_sync(1, 128);  // the staging block may be rewritten
       };
+      // TMEM blocks are double-buffered in registers: block j+1's tcgen05.ld is in flight while block
+      // j is converted and stored (fully unrolled, so the buffer index is static).
       if (EPI == TEPI_STORE) {
-#pragma unroll 1
+        uint32_t r[2][32];
+        tmem_ld32(taddr, r[0]);
+        tmem_ld_wait();
+#pragma unroll
         for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_ld_wait();
+          const int bi = (c / 32) & 1;
+          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
           float y[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) y[e] = alpha * __uint_as_float(r[e]);
+          for (int e = 0; e < 32; ++e) y[e] = alpha * __uint_as_float(r[bi][e]);
           if (ea.Cf) emit(c / 32, y, true);
           if (ea.Cs) emit(c / 32, y, false);
+          tmem_ld_wait();
         }
       } else if (EPI == TEPI_SWIGLU) {
-#pragma unroll 1
+        uint32_t u[2][32], v[2][32];
+        tmem_ld32(taddr, u[0]);
+        tmem_ld32(taddr + 32, v[0]);
+        tmem_ld_wait();
+#pragma unroll
         for (int c = 0; c < BN; c += 64) {
-          uint32_t u[32], v[32];
-          tmem_ld32(taddr + c, u);
-          tmem_ld32(taddr + c + 32, v);
-          tmem_ld_wait();
+          const int bi = (c / 64) & 1;
+          if (c + 64 < BN) {
+            tmem_ld32(taddr + c + 64, u[bi ^ 1]);
+            tmem_ld32(taddr + c + 96, v[bi ^ 1]);
+          }
           float y[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(u[e]) * silu_f(__uint_as_float(v[e]));
+          for (int e = 0; e < 32; ++e) y[e] = swiglu_f(__uint_as_float(u[bi][e]), __uint_as_float(v[bi][e]));
           emit(c / 64, y, false);
+          tmem_ld_wait();
         }
       } else {  // TEPI_LN over BN == d columns
-        float sum = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_ld_wait();
+        // one statistics pass, sums shifted by the row's first value (no cancellation for rows whose
+        // mean is large against their spread): mu = x0 + S1/n, var = S2/n - (S1/n)^2 (biased)
+        uint32_t r[2][32];
+        tmem_ld32(taddr, r[0]);
+        tmem_ld_wait();
+        const float x0 = __uint_as_float(r[0][0]);
+        float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) sum += __uint_as_float(r[e]);
-        }
-        const float mu = sum / BN;
-        float v2 = 0.f;
-#pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_ld_wait();
+          const int bi = (c / 32) & 1;
+          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const float d0 = __uint_as_float(r[e]) - mu;
-            v2 += d0 * d0;
+            const float d0 = __uint_as_float(r[bi][e]) - x0;
+            s1 += d0;
+            s2 = fmaf(d0, d0, s2);
           }
-        }
-        const float inv = rsqrtf(v2 / BN + ea.eps);
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
           tmem_ld_wait();
+        }
+        const float m1 = s1 / BN, mu = x0 + m1;
+        const float inv = rsqrtf(fmaxf(s2 / BN - m1 * m1, 0.f) + ea.eps);
+        tmem_ld32(taddr, r[0]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) {
+          const int bi = (c / 32) & 1;
+          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
           float y[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            y[e] = (__uint_as_float(r[e]) - mu) * inv * __ldg(ea.g + c + e) + __ldg(ea.b + c + e);
+          for (int e = 0; e < 32; e += 4) {
+            const float4 g4 = *reinterpret_cast<const float4 *>(lnp + c + e);
+            const float4 b4 = *reinterpret_cast<const float4 *>(lnp + BN + c + e);
+            y[e] = fmaf((__uint_as_float(r[bi][e]) - mu) * inv, g4.x, b4.x);
+            y[e + 1] = fmaf((__uint_as_float(r[bi][e + 1]) - mu) * inv, g4.y, b4.y);
+            y[e + 2] = fmaf((__uint_as_float(r[bi][e + 2]) - mu) * inv, g4.z, b4.z);
+            y[e + 3] = fmaf((__uint_as_float(r[bi][e + 3]) - mu) * inv, g4.w, b4.w);
+          }
           if (ea.Cf) emit(c / 32, y, true);
           if (ea.Cs) emit(c / 32, y, false);
+          tmem_ld_wait();
         }
       }
       static_assert(OUT_COLS >= 32 || EPI == TEPI_SWIGLU, "32-column output blocks");
