@@ -56,12 +56,13 @@ struct GemmCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int F_STRIDE = 32 * 4 + 16;    // staged fp32 row of a 32-column output block (bytes)
   static constexpr int H_STRIDE = 32 * 2 + 16;    // staged bf16 row
-  static constexpr int STG_BYTES = 128 * F_STRIDE;  // one staged output block (dedicated: the ring keeps running)
-  static constexpr int STAGES = (200 * 1024 / STAGE) > 6 ? 6 : (200 * 1024 / STAGE);
+  static constexpr int STG_BYTES = 128 * F_STRIDE;  // one staged output block per epilogue half (the ring keeps running)
+  static constexpr int LNP_BYTES = 2 * BN * 4 + 2 * 128 * 8;  // LayerNorm gamma | beta, half-row statistics
+  static constexpr int STAGES_FIT = (227 * 1024 - 2 * STG_BYTES - LNP_BYTES - 1024 - 256) / STAGE;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
   static constexpr int NACC = TMEM_COLS <= 256 ? 2 : 1;  // TMEM accumulators (double-buffered when they fit)
-  static constexpr int LNP_BYTES = 2 * BN * 4;     // LayerNorm gamma | beta, staged once per CTA
-  static constexpr int SMEM = STAGES * STAGE + STG_BYTES + LNP_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + 2 * STG_BYTES + LNP_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // PERSISTENT: grid = 2 x min(tile pairs, co-resident clusters); cluster c takes 256-row tile pairs
@@ -70,19 +71,22 @@ struct GemmCfg {
 // i (TMEM -> registers -> padded smem block -> coalesced 16-byte stores) overlaps the MMAs of tile
 // i+1 and the loads of tile i+2; per-tile launch / prologue / pipeline-fill costs are paid once
 // per SM instead of once per tile (these GEMMs are small: M = N_t = 16384 rows).
+constexpr int GEMM_THREADS = 320;  // epilogue warps 0-7, TMA producer 8, MMA issuer 9
+
 template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
               int K, float alpha, EpiArgs ea) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *stg = smem + C::STAGES * C::STAGE;
-  float *lnp = reinterpret_cast<float *>(stg + C::STG_BYTES);  // LN: gamma [BN] | beta [BN]
-  uint64_t *full = reinterpret_cast<uint64_t *>(stg + C::STG_BYTES + C::LNP_BYTES);
+  float *lnp = reinterpret_cast<float *>(stg + 2 * C::STG_BYTES);  // LN: gamma [BN] | beta [BN]
+  float2 *lnx = reinterpret_cast<float2 *>(lnp + 2 * BN);           // LN: (mean, M2) of each half row
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + 2 * C::STG_BYTES + C::LNP_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *acc_full = empty + C::STAGES;   // NACC (MMA commit: accumulator a complete)
-  uint64_t *acc_empty = acc_full + 2;       // NACC, leader only (8 epilogue warps of the pair: accumulator a read)
+  uint64_t *acc_empty = acc_full + 2;       // NACC, leader only (16 epilogue warps of the pair: accumulator a read)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -91,13 +95,13 @@ __global__ void __launch_bounds__(192, 1)
   // SM receives 16 KB of A + BN/2 x 64 x 2 bytes of B per 64-deep k-block instead of the whole B —
   // per-SM operand ingest, not L2, is what limits M = 128 tiles at BN >= 256 (a 2-CTA TMA multicast
   // of B measured within 2%: every SM still receives all of B).
-    // Tile pairs are numbered n-fastest: the pairs in flight share a few 256-row blocks of A (read
+  // Tile pairs are numbered n-fastest: the pairs in flight share a few 256-row blocks of A (read
   // from HBM once) and sweep all of B (the weights, L2-resident).
   const int tiles_m = (M + C::BM - 1) / C::BM, tn = N / BN, npairs = (tiles_m + 1) / 2 * tn;
   const int nk = (K + C::BK - 1) / C::BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch(&mapA);
     tma_prefetch(&mapB);
     for (int s = 0; s < C::STAGES; ++s) {
@@ -106,11 +110,11 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 8);
+      mbar_init(&acc_empty[a], 16);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc_pair(tslot, C::NACC * C::TMEM_COLS);
+  if (warp == 9) tmem_alloc_pair(tslot, C::NACC * C::TMEM_COLS);
   tc_fence_before();
   cluster_sync_all();  // barrier inits visible cluster-wide before the peer multicasts into this CTA
   tc_fence_after();
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(192, 1)
   pdl_wait();     // the predecessor's outputs (our A) are complete and visible
   pdl_trigger();  // the successor may be scheduled (it waits for us the same way)
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {  // TMA producer
       int s = 0, ph = 0;
       for (int p = cid; p < npairs; p += ncl) {
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0 && crank == 0) {  // MMA issuer (the pair's leader)
       constexpr uint32_t idesc = idesc_bf16(256, C::NS, 0);
       int s = 0, ph = 0, i = 0;
@@ -166,19 +170,27 @@ __global__ void __launch_bounds__(192, 1)
         umma_commit_pair_mc(&acc_full[a], 0x3);  // both CTAs' accumulator halves are complete
       }
     }
-  } else {  // epilogue warps 0..3: TMEM lane quarter = warp
-    // Each 32-column output block is staged in shared memory with padded rows, then copied out by
-    // all 128 threads with coalesced 16-byte stores (a row per thread written straight to global
-    // touches 32 sectors per store instruction).
-    const int q = warp & 3;
+  } else {  // epilogue warps 0..7: TMEM lane quarter = warp & 3, column half hg = warp >> 2
+    // Each half group (4 warps, 128 threads: all 128 rows, half of the columns) stages a 32-column
+    // output block in its own SMEM buffer with padded rows and copies it out with coalesced 16-byte
+    // stores (a row per thread written straight to global touches 32 sectors per store).  Two
+    // warps per TMEM lane quarter halve the epilogue, which bounds NACC = 1 tiles (BN = 512).
+    const int q = warp & 3, hg = warp >> 2, ltid = threadIdx.x & 127;
     const int row = q * 32 + lane;
+    uint8_t *hstg = stg + hg * C::STG_BYTES;
+    // columns of the accumulator this half group owns (a half group may own none for tiny BN)
+    constexpr int GRAN = EPI == TEPI_SWIGLU ? 64 : 32;
+    constexpr bool SPLIT = BN >= 2 * GRAN;
+    constexpr int HCOLS = SPLIT ? BN / 2 : BN;
+    const int c_lo = SPLIT ? hg * HCOLS : 0;
+    const bool active = SPLIT || hg == 0;
     constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
     if (EPI == TEPI_LN) {  // gamma/beta from SMEM: global loads in flight stall this warp's tcgen05.ld
-      for (int c = threadIdx.x; c < BN; c += 128) {
+      for (int c = threadIdx.x; c < BN; c += 256) {
         lnp[c] = ea.g[c];
         lnp[BN + c] = ea.b[c];
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(3, 256);
     }
     int i = 0;
     for (int p = cid; p < npairs; p += ncl, ++i) {
@@ -187,11 +199,11 @@ __global__ void __launch_bounds__(192, 1)
       const int a = i % C::NACC;
       mbar_wait(&acc_full[a], (i / C::NACC) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem + a * C::TMEM_COLS + ((uint32_t)(q * 32) << 16);
-      // stage block `blk` (32 output columns, fp32 or bf16 rows), then store it coalesced
+      const uint32_t taddr = tmem + a * C::TMEM_COLS + ((uint32_t)(q * 32) << 16) + c_lo;
+      // stage output block `blk` (32 output columns of the tile, fp32 or bf16 rows), then store it
       auto emit = [&](int blk, const float (&y)[32], bool f32) {
-        const int RS = f32 ? C::F_STRIDE : C::H_STRIDE, BW = f32 ? 128 : 64, ES = f32 ? 4 : 2;
-        uint8_t *srow = stg + row * RS;
+        const int RS = f32 ? C::F_STRIDE : C::H_STRIDE, ES = f32 ? 4 : 2;
+        uint8_t *srow = hstg + row * RS;
         if (f32) {
 #pragma unroll
           for (int k = 0; k < 8; ++k)
@@ -203,65 +215,71 @@ __global__ void __launch_bounds__(192, 1)
                 make_uint4(pack_bf16(y[8 * k], y[8 * k + 1]), pack_bf16(y[8 * k + 2], y[8 * k + 3]),
                            pack_bf16(y[8 * k + 4], y[8 * k + 5]), pack_bf16(y[8 * k + 6], y[8 * k + 7]));
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1 + hg, 128);
         uint8_t *dst = f32 ? reinterpret_cast<uint8_t *>(ea.Cf) : reinterpret_cast<uint8_t *>(ea.Cs);
         const int64_t ld = f32 ? ea.ldcf : ea.ldcs;
-        const int per_row = BW / 16;
-        for (int c = threadIdx.x; c < 128 * per_row; c += 128) {
-          const int rr = c / per_row, ch = c % per_row;
+        const int sh = f32 ? 3 : 2;  // log2(16-byte chunks per staged row)
+#pragma unroll 4
+        for (int c = ltid; c < (128 << sh); c += 128) {
+          const int rr = c >> sh, ch = c & ((1 << sh) - 1);
           if ((int64_t)m0 + rr < M)
             *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + out_n0 + blk * 32) * ES + ch * 16) =
-                *reinterpret_cast<const uint4 *>(stg + rr * RS + ch * 16);
+                *reinterpret_cast<const uint4 *>(hstg + rr * RS + ch * 16);
         }
-        named_bar_sync(1, 128);  // the staging block may be rewritten
+        named_bar_sync(1 + hg, 128);  // the staging block may be rewritten
       };
       // TMEM blocks are double-buffered in registers: block j+1's tcgen05.ld is in flight while block
       // j is converted and stored (fully unrolled, so the buffer index is static).
       if (EPI == TEPI_STORE) {
-        uint32_t r[2][32];
-        tmem_ld32(taddr, r[0]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          const int bi = (c / 32) & 1;
-          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
-          float y[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) y[e] = alpha * __uint_as_float(r[bi][e]);
-          if (ea.Cf) emit(c / 32, y, true);
-          if (ea.Cs) emit(c / 32, y, false);
+        if (active) {
+          uint32_t r[2][32];
+          tmem_ld32(taddr, r[0]);
           tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < HCOLS; c += 32) {
+            const int bi = (c / 32) & 1;
+            if (c + 32 < HCOLS) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
+            float y[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) y[e] = alpha * __uint_as_float(r[bi][e]);
+            if (ea.Cf) emit((c_lo + c) / 32, y, true);
+            if (ea.Cs) emit((c_lo + c) / 32, y, false);
+            tmem_ld_wait();
+          }
         }
       } else if (EPI == TEPI_SWIGLU) {
-        uint32_t u[2][32], v[2][32];
-        tmem_ld32(taddr, u[0]);
-        tmem_ld32(taddr + 32, v[0]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < BN; c += 64) {
-          const int bi = (c / 64) & 1;
-          if (c + 64 < BN) {
-            tmem_ld32(taddr + c + 64, u[bi ^ 1]);
-            tmem_ld32(taddr + c + 96, v[bi ^ 1]);
-          }
-          float y[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) y[e] = swiglu_f(__uint_as_float(u[bi][e]), __uint_as_float(v[bi][e]));
-          emit(c / 64, y, false);
+        if (active) {
+          uint32_t u[2][32], v[2][32];
+          tmem_ld32(taddr, u[0]);
+          tmem_ld32(taddr + 32, v[0]);
           tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < HCOLS; c += 64) {
+            const int bi = (c / 64) & 1;
+            if (c + 64 < HCOLS) {
+              tmem_ld32(taddr + c + 64, u[bi ^ 1]);
+              tmem_ld32(taddr + c + 96, v[bi ^ 1]);
+            }
+            float y[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) y[e] = swiglu_f(__uint_as_float(u[bi][e]), __uint_as_float(v[bi][e]));
+            emit((c_lo + c) / 64, y, false);
+            tmem_ld_wait();
+          }
         }
-      } else {  // TEPI_LN over BN == d columns
-        // one statistics pass, sums shifted by the row's first value (no cancellation for rows whose
-        // mean is large against their spread): mu = x0 + S1/n, var = S2/n - (S1/n)^2 (biased)
+      } else if (active) {  // TEPI_LN over BN == d columns
+        // one statistics pass over the half row, sums shifted by its first value (no cancellation
+        // for rows whose mean is large against their spread); the halves' (mean, M2) combine as
+        // mean = (m_0 + m_1)/2, M2 = M2_0 + M2_1 + (m_0 - m_1)^2 n/4 (n = BN, equal halves)
         uint32_t r[2][32];
         tmem_ld32(taddr, r[0]);
         tmem_ld_wait();
         const float x0 = __uint_as_float(r[0][0]);
         float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < HCOLS; c += 32) {
           const int bi = (c / 32) & 1;
-          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
+          if (c + 32 < HCOLS) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const float d0 = __uint_as_float(r[bi][e]) - x0;
@@ -270,28 +288,41 @@ __global__ void __launch_bounds__(192, 1)
           }
           tmem_ld_wait();
         }
-        const float m1 = s1 / BN, mu = x0 + m1;
-        const float inv = rsqrtf(fmaxf(s2 / BN - m1 * m1, 0.f) + ea.eps);
-        tmem_ld32(taddr, r[0]);
+        tmem_ld32(taddr, r[0]);  // first block of the output pass, in flight during the exchange
+        const float mh = x0 + s1 / HCOLS, m2h = fmaxf(s2 - s1 * (s1 / HCOLS), 0.f);
+        float mu, var;
+        if (SPLIT) {
+          lnx[hg * 128 + row] = make_float2(mh, m2h);
+          named_bar_sync(3, 256);
+          const float2 o = lnx[(hg ^ 1) * 128 + row];
+          const float dm = mh - o.x;
+          mu = 0.5f * (mh + o.x);
+          var = (m2h + o.y + dm * dm * (0.25f * BN)) / BN;
+        } else {
+          mu = mh;
+          var = m2h / BN;
+        }
+        const float inv = rsqrtf(var + ea.eps);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < HCOLS; c += 32) {
           const int bi = (c / 32) & 1;
-          if (c + 32 < BN) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
+          if (c + 32 < HCOLS) tmem_ld32(taddr + c + 32, r[bi ^ 1]);
           float y[32];
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            const float4 g4 = *reinterpret_cast<const float4 *>(lnp + c + e);
-            const float4 b4 = *reinterpret_cast<const float4 *>(lnp + BN + c + e);
+            const float4 g4 = *reinterpret_cast<const float4 *>(lnp + c_lo + c + e);
+            const float4 b4 = *reinterpret_cast<const float4 *>(lnp + BN + c_lo + c + e);
             y[e] = fmaf((__uint_as_float(r[bi][e]) - mu) * inv, g4.x, b4.x);
             y[e + 1] = fmaf((__uint_as_float(r[bi][e + 1]) - mu) * inv, g4.y, b4.y);
             y[e + 2] = fmaf((__uint_as_float(r[bi][e + 2]) - mu) * inv, g4.z, b4.z);
             y[e + 3] = fmaf((__uint_as_float(r[bi][e + 3]) - mu) * inv, g4.w, b4.w);
           }
-          if (ea.Cf) emit(c / 32, y, true);
-          if (ea.Cs) emit(c / 32, y, false);
+          if (ea.Cf) emit((c_lo + c) / 32, y, true);
+          if (ea.Cs) emit((c_lo + c) / 32, y, false);
           tmem_ld_wait();
         }
+        if (SPLIT) named_bar_sync(3, 256);  // lnx of this tile consumed before the next tile writes it
       }
       static_assert(OUT_COLS >= 32 || EPI == TEPI_SWIGLU, "32-column output blocks");
       tc_fence_before();
@@ -301,7 +332,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   cluster_sync_all();  // the peer no longer multicasts into / arrives on this CTA
-  if (warp == 5) tmem_dealloc_pair(tmem, C::NACC * C::TMEM_COLS);
+  if (warp == 9) tmem_dealloc_pair(tmem, C::NACC * C::TMEM_COLS);
 }
 
 // bf16 [n2 x n1 x n0] (n0 innermost, contiguous), box = box1 rows x 64 x 1, SWIZZLE_128B
@@ -367,7 +398,7 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
   if (!mc) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(GEMM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cudaLaunchAttribute ca[1];
     ca[0].id = cudaLaunchAttributeClusterDimension;
@@ -388,7 +419,7 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
   note_launch();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(npairs, mc)));
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
