@@ -50,7 +50,8 @@ def test_tc_gemm_store(M, N, K):
     assert (Cs.float() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
 
 
-@pytest.mark.parametrize("M,d,rd", [(300, 128, 512), (128, 64, 256), (513, 256, 1024)])
+@pytest.mark.parametrize("M,d,rd", [(300, 128, 512), (128, 64, 256), (513, 256, 1024),
+                                    (40000, 512, 2048)])  # BN = 512: one accumulator, clusters loop
 def test_tc_gemm_swiglu_and_ln(M, d, rd):
     import torch
     torch.manual_seed(1)
@@ -76,3 +77,25 @@ def test_tc_gemm_swiglu_and_ln(M, d, rd):
     ref = torch.nn.functional.layer_norm(H.float() @ Wo.float(), (d,), g, b, eps=1e-5)
     assert (outf - ref).abs().max().item() < 1e-3
     assert (out.float() - ref).abs().max().item() < 3e-2
+
+
+@pytest.mark.parametrize("d", [128, 512])
+def test_tc_gemm_ln_offset_rows(d):
+    """LayerNorm epilogue on rows whose mean is ~100x their spread (the statistics are one pass of
+    sums shifted by the row's first value, then the two column halves are combined): the result must
+    still match a two-pass fp32 LayerNorm of the same fp32 accumulator."""
+    import torch
+    torch.manual_seed(3)
+    M, K = 1000, 256
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    base = torch.randn(K, device="cuda")
+    Bt = (base[None, :] + 0.01 * torch.randn(d, K, device="cuda")).bfloat16()
+    g = 1 + 0.1 * torch.randn(d, device="cuda")
+    b = 0.1 * torch.randn(d, device="cuda")
+    outf = torch.zeros(M, d, device="cuda")
+    _gemm(2, A, Bt, Cf=outf, g=g, b=b)
+    Y = A.double() @ Bt.double().T
+    ref = torch.nn.functional.layer_norm(Y, (d,), g.double(), b.double(), eps=1e-5).float()
+    spread = (Y - Y.mean(1, keepdim=True)).abs().mean().item() / Y.abs().mean().item()
+    assert spread < 0.05, spread  # the rows really are offset-dominated
+    assert (outf - ref).abs().max().item() < 2e-2
