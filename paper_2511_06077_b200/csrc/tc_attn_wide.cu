@@ -9,19 +9,27 @@
 //                                   of S = U X~^T, d/2 packed columns)
 //   upper lane half (lane base 16): O (d columns)
 // P goes through shared memory (SW128 K-major) as the A operand of O += P X~ (SS mode; a TS
-// operand must share the accumulator's lane half).  The softmax is two-pass: pass 0 streams the
-// key tiles once for the exact row maxima, pass 1 recomputes S and accumulates P X~, so O is never
-// rescaled.  X~ tiles of 64 keys (d/64 boxes of 64 columns, 3-4 stage TMA ring) serve as the
-// K-major B of S and the MN-major B of PV.
+// operand must share the accumulator's lane half).  The softmax is ONE pass with a lazy running
+// maximum: a row keeps its reference maximum m until a key tile's maximum exceeds it by more than
+// 2^8 (P <= 256 is still exact enough in bf16 and the fp32 sums), and only then rescales its O row
+// and l in place after the PV MMAs issued so far have completed — rare after the first tile, so
+// S = U X~^T is computed once per key tile (the earlier two-pass form recomputed it: 3 MMA
+// passes for 2 useful ones).  X~ tiles of 64 keys (d/64 boxes of 64 columns, 3-4 stage TMA ring)
+// serve as the K-major B of S and the MN-major B of PV.
 //
-// Warp roles (352 threads): 0..7 softmax (lanes 0-15 of each warp: one S row, half of the 64 key
-// columns per warp pair) and epilogue (lanes 16-31: one O row, half of the d columns), 8 TMA
-// producer, 9 TMEM allocator + S issuer, 10 PV issuer.
+// Warp roles (352 threads): 0..3 softmax on the 16x32bx2 TMEM shape (threads t and t+16 share S
+// row t of the warp's lane quarter, 32 key columns each; the row max is one shuffle) and O
+// rescale; 0..7 load U and write the output (two warps per lane quarter, a quarter of the O
+// columns each); 8 TMA producer, 9 TMEM allocator + S issuer, 10 PV issuer.
 #include <math.h>
 
 #include "launch.h"
 #include "tc.h"
 #include "tc_ptx.cuh"
+
+#ifndef STCA_WIDE_LAZY
+#define STCA_WIDE_LAZY 8.f  // rescale threshold in log2 units (a test build sets 0: rescale on every increase)
+#endif
 
 namespace stca {
 namespace tc {
@@ -34,7 +42,7 @@ struct WCfg {
   static constexpr int X_BYTES = BN * D * 2;             // d/64 boxes of 64 x 64 (8 KB)
   static constexpr int STAGES = D == 512 ? 3 : 4;
   static constexpr int P_BYTES = BM * BN * 2;            // 8 KB, SW128 K-major
-  static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + 2 * 2 * 64 * 4 + 256;
+  static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + 2 * 64 * 4 + 256;
   static constexpr uint32_t TS = 0, TU = 256;            // lower lane half: S0 | S1 ... U
   static constexpr uint32_t TO = 16u << 16;              // upper lane half: O
 };
@@ -48,15 +56,15 @@ __global__ void __launch_bounds__(352, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sX = smem;
   uint8_t *sP = sX + C::STAGES * C::X_BYTES;
-  float *sMax = reinterpret_cast<float *>(sP + 2 * C::P_BYTES);  // [half][64]
-  float *sSum = sMax + 2 * 64;                                   // [half][64]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sSum + 2 * 64);
+  float *sM = reinterpret_cast<float *>(sP + 2 * C::P_BYTES);  // [64] reference maximum per row
+  float *sL = sM + 64;                                         // [64] sum per row
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sL + 64);
   uint64_t *u_full = bar;                      // 8 warp arrivals
   uint64_t *x_full = bar + 1;                  // STAGES
-  uint64_t *x_empty = x_full + C::STAGES;      // STAGES
+  uint64_t *x_empty = x_full + C::STAGES;      // STAGES (PV commit)
   uint64_t *s_full = x_empty + C::STAGES;      // 2
-  uint64_t *s_free = s_full + 2;               // 2 (8 warp arrivals)
-  uint64_t *p_full = s_free + 2;               // 2 (8 warp arrivals)
+  uint64_t *s_free = s_full + 2;               // 2 (4 softmax warps)
+  uint64_t *p_full = s_free + 2;               // 2 (4 softmax warps)
   uint64_t *pv_done = p_full + 2;              // 2
   uint32_t *tslot = reinterpret_cast<uint32_t *>(pv_done + 2);
 
@@ -73,8 +81,8 @@ __global__ void __launch_bounds__(352, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_free[b], 8);
-      mbar_init(&p_full[b], 8);
+      mbar_init(&s_free[b], 4);
+      mbar_init(&p_full[b], 4);
       mbar_init(&pv_done[b], 1);
     }
     fence_mbar_init();
@@ -86,30 +94,28 @@ __global__ void __launch_bounds__(352, 1)
   const uint32_t tmem = *tslot;
 
   if (warp == 8) {
-    if (lane == 0) {  // ---------------- TMA producer: 2 passes over the key tiles ----------------
-      const uint64_t pol = policy_evict_last();  // the second pass re-reads the chunk from L2
+    if (lane == 0) {  // ---------------- TMA producer: the key tiles, once ----------------
       int s = 0, ph = 0;
-      for (int g = 0; g < 2 * nt; ++g) {
-        const int j = g < nt ? g : g - nt;
+      for (int j = 0; j < nt; ++j) {
         mbar_wait(&x_empty[s], ph ^ 1);
         uint8_t *dst = sX + s * C::X_BYTES;
         const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BN);
         mbar_expect_tx(&x_full[s], C::X_BYTES);
 #pragma unroll
-        for (int bx = 0; bx < D / 64; ++bx) tma_load_2d_hint(dst + bx * 8192, &mapX, &x_full[s], 64 * bx, row, pol);
+        for (int bx = 0; bx < D / 64; ++bx) tma_load_2d(dst + bx * 8192, &mapX, &x_full[s], 64 * bx, row);
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- S issuer: S_g = U X~^T (TS, M = 64, N = 64) ----------------
+    if (lane == 0) {  // ---------------- S issuer: S_j = U X~_j^T (TS, M = 64, N = 64) ----------------
       constexpr uint32_t idesc_s = idesc_bf16(64, C::BN, 0);
       const uint32_t aX = smem_u32(sX);
       mbar_wait(u_full, 0);
       int s = 0, ph = 0;
-      for (int g = 0; g < 2 * nt; ++g) {
-        const int b = g & 1;
+      for (int j = 0; j < nt; ++j) {
+        const int b = j & 1;
         mbar_wait(&x_full[s], ph);
-        if (g >= 2) mbar_wait(&s_free[b], ((g - 2) >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
         tc_fence_after();
         const uint32_t xs = aX + s * C::X_BYTES;
 #pragma unroll 8
@@ -117,19 +123,18 @@ __global__ void __launch_bounds__(352, 1)
           umma_f16_ts(tmem + C::TS + b * C::BN, tmem + C::TU + k * 8,
                       sdesc_sw128(xs + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024), idesc_s, k != 0);
         umma_commit(&s_full[b]);
-        if (g < nt) umma_commit(&x_empty[s]);  // pass 0: no PV reads this stage
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 10) {
-    if (lane == 0) {  // ---------------- PV issuer (pass 1): O += P X~ (SS, M = 64, N <= 256) ----------------
+    if (lane == 0) {  // ---------------- PV issuer: O += P_j X~_j (SS, M = 64, N <= 256) ----------------
       constexpr int NS = D < 256 ? D : 256;
       constexpr uint32_t idesc_o = idesc_bf16(64, NS, 1);
       const uint32_t aX = smem_u32(sX), aP = smem_u32(sP);
-      int s = nt % C::STAGES, ph = (nt / C::STAGES) & 1;  // the ring position of tile g = nt
+      int s = 0;
       for (int j = 0; j < nt; ++j) {
         const int b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
+        mbar_wait(&p_full[b], (j >> 1) & 1);  // P_j written (and O rescaled, if it had to be)
         tc_fence_after();
         const uint32_t xs = aX + s * C::X_BYTES, ps = aP + b * C::P_BYTES;
 #pragma unroll
@@ -142,19 +147,17 @@ __global__ void __launch_bounds__(352, 1)
         }
         umma_commit(&pv_done[b]);
         umma_commit(&x_empty[s]);
-        if (++s == C::STAGES) { s = 0; ph ^= 1; }
-        (void)ph;
+        if (++s == C::STAGES) s = 0;
       }
     }
-  } else {  // ---------------- softmax (lanes 0-15) / epilogue (lanes 16-31), warps 0..7 ----------------
+  } else {  // ---------------- warps 0..7: U load; 0..3 softmax; 0..7 output ----------------
     const int q = warp & 3, hh = warp >> 2;
-    const bool srow = lane < 16;
-    const int r = q * 16 + (lane & 15);  // the S row (lanes 0-15) or O row (lanes 16-31) of this thread
-    const uint32_t qoff = (uint32_t)(q * 32) << 16;
     {  // U row -> TMEM lower half (the A operand of S); lanes 16-31 write zeros into the upper half
+      const int r = q * 16 + (lane & 15);
       const int64_t grow = it.qrow0 + r;
-      const bool ld = srow && grow < NQ;
+      const bool ld = lane < 16 && grow < NQ;
       const uint4 *src = reinterpret_cast<const uint4 *>(U + grow * D + (D / 2) * hh);
+      const uint32_t qoff = (uint32_t)(q * 32) << 16;
 #pragma unroll
       for (int c = 0; c < D / 4; c += 16) {  // this half's D/2 bf16 = D/4 packed columns
         uint32_t w[16];
@@ -173,97 +176,108 @@ __global__ void __launch_bounds__(352, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(u_full);
     }
-    // ---- pass 0: exact row maxima ----
-    float mpart = -INFINITY;
-    for (int j = 0; j < nt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[32];
-      tmem_ld32(tmem + qoff + C::TS + b * C::BN + 32 * hh, sr);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
-      const int kvalid = it.klen - j * C::BN - 32 * hh;
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    // 16x32bx2 view of lane quarter q: thread t and t+16 <-> query row q*16 + (t & 15)
+    const int pp = lane >> 4, r = q * 16 + (lane & 15);
+    const uint32_t s_lanes = (uint32_t)(q * 32) << 16, o_lanes = (uint32_t)(q * 32 + 16) << 16;
+    if (warp < 4) {
+      float m_ref = -INFINITY, l = 0.f;  // identical in both threads of the row
+      for (int j = 0; j < nt; ++j) {
+        const int b = j & 1;
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[32];
+        tmem_ld16x2_32<32>(tmem + s_lanes + C::TS + b * C::BN, sr);  // t: keys 0-31, t+16: keys 32-63
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[b]);
+        const int kvalid = it.klen - j * C::BN - 32 * pp;
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c < kvalid) mx[c & 3] = fmaxf(mx[c & 3], __uint_as_float(sr[c]));
-      mpart = fmaxf(mpart, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
-    }
-    if (srow) sMax[hh * 64 + r] = mpart;
-    named_bar_sync(1, 256);
-    const float m = fmaxf(sMax[r], sMax[64 + r]);  // valid for the S-row lanes
-    // ---- pass 1: P = 2^(S - m) into shared memory, O += P X~ ----
-    float lpart = 0.f;
-    for (int j = 0; j < nt; ++j) {
-      const int g = nt + j, b = g & 1, pb = j & 1;
-      mbar_wait(&s_full[b], (g >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[32];
-      tmem_ld32(tmem + qoff + C::TS + b * C::BN + 32 * hh, sr);
-      tmem_ld_wait();
-      const int kvalid = it.klen - j * C::BN - 32 * hh;
-      if (j >= 2) mbar_wait(&pv_done[pb], ((j - 2) >> 1) & 1);  // PV of tile j-2 has read P buffer pb
-      uint32_t w[16];
+        for (int c = 0; c < 32; ++c)
+          if (c < kvalid) mx[c & 3] = fmaxf(mx[c & 3], __uint_as_float(sr[c]));
+        float tm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+        if (j == 0) {
+          m_ref = tm;  // tile 0 always holds a valid key of the item
+        } else {
+          const bool need = tm > m_ref + STCA_WIDE_LAZY;
+          if (__any_sync(0xffffffffu, need)) {  // rescale this warp's O rows once the PVs so far are done
+            mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+            tc_fence_after();
+            const float f = need ? ex2(m_ref - tm) : 1.f;
+            if (need) {
+              l *= f;
+              m_ref = tm;
+            }
+#pragma unroll 1
+            for (int c = 0; c < D / 2; c += 32) {  // t: columns [c, c+32), t+16: [D/2 + c, D/2 + c + 32)
+              uint32_t o[32];
+              tmem_ld16x2_32<D / 2>(tmem + o_lanes + c, o);
+              tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float p0 = 2 * i < kvalid ? ex2(__uint_as_float(sr[2 * i]) - m) : 0.f;
-        const float p1 = 2 * i + 1 < kvalid ? ex2(__uint_as_float(sr[2 * i + 1]) - m) : 0.f;
-        w[i] = pack_bf16(p0, p1);
-        lpart += p0 + p1;
-      }
-      if (srow) {
-        uint8_t *pr = sP + pb * C::P_BYTES;
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+              tmem_st16x2_32<D / 2>(tmem + o_lanes + c, o);
+            }
+            tmem_st_wait();
+          }
+        }
+        const int pb = j & 1;
+        if (j >= 2) mbar_wait(&pv_done[pb], ((j - 2) >> 1) & 1);  // PV of tile j-2 has read P buffer pb
+        uint32_t w[16];
+        float lsum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = 2 * i < kvalid ? ex2(__uint_as_float(sr[2 * i]) - m_ref) : 0.f;
+          const float p1 = 2 * i + 1 < kvalid ? ex2(__uint_as_float(sr[2 * i + 1]) - m_ref) : 0.f;
+          w[i] = pack_bf16(p0, p1);
+          lsum += p0 + p1;
+        }
+        l += lsum;
+        uint8_t *prow = sP + pb * C::P_BYTES;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          *reinterpret_cast<uint4 *>(pr + sw128_off(r, 4 * hh + k)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          *reinterpret_cast<uint4 *>(prow + sw128_off(r, 4 * pp + k)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
       }
-      fence_proxy_async();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_free[b]);
-        mbar_arrive(&p_full[pb]);
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      if (pp == 0) {
+        sM[r] = m_ref;
+        sL[r] = l;
       }
     }
-    if (srow) sSum[hh * 64 + r] = lpart;
-    if (nt >= 1) mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
-    tc_fence_after();
+    // the softmax warps (in step with pv_done) wait for the last PV; warps 4-7 would be phases ahead
+    if (warp < 4 && nt >= 1) mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
+    tc_fence_before();
     named_bar_sync(1, 256);
-    // ---- epilogue: lanes 16-31 own O row r (upper lane half); this warp writes d/2 of its columns ----
-    const float l = sSum[r] + sSum[64 + r];
-    const bool ok = !srow && r < it.nq;
+    tc_fence_after();
+    // ---- output: warp (q, hh) writes columns [hh D/4, (hh+1) D/4) (t) and D/2 + that (t+16) of its rows ----
+    const float l = sL[r], inv = 1.f / l;
+    const bool ok = r < it.nq;
 #pragma unroll 1
-    for (int c = 0; c < D / 2; c += 32) {
+    for (int c = hh * (D / 4); c < (hh + 1) * (D / 4); c += 32) {
       uint32_t o[32];
-      tmem_ld32(tmem + qoff + (D / 2) * hh + c, o);  // lanes 16-31 read the upper half = O
+      tmem_ld16x2_32<D / 2>(tmem + o_lanes + c, o);
       tmem_ld_wait();
       if (ok) {
-        const int col = (D / 2) * hh + c;
+        const int col = c + pp * (D / 2);
+        uint4 *dst;
         if (it.part_row < 0) {
-          const float inv = 1.f / l;
-          uint4 *dst = reinterpret_cast<uint4 *>(Y + (it.qrow0 + r) * D + col);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
-        } else {
+          dst = reinterpret_cast<uint4 *>(Y + (it.qrow0 + r) * D + col);
+        } else {  // partials hold the chunk's normalised output O / l, then (m, l)
           uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + r) * (int64_t)part_row_bytes(D, 2);
-          if (col == 0)
-            *reinterpret_cast<float2 *>(pr + 2 * D) = make_float2(sMax[r] > sMax[64 + r] ? sMax[r] : sMax[64 + r], l);
-          const float inv = 1.f / l;  // partials hold the chunk's normalised output O / l
-          uint4 *dst = reinterpret_cast<uint4 *>(pr + 2 * col);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
+          if (col == 0) *reinterpret_cast<float2 *>(pr + 2 * D) = make_float2(sM[r], l);
+          dst = reinterpret_cast<uint4 *>(pr + 2 * col);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                              pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
       }
     }
   }

@@ -81,6 +81,15 @@ def test_bf16_sharp_softmax():
     check(wl, Z, z, TOL["bf16"])
 
 
+@pytest.mark.parametrize("d,h", [(256, 8), (512, 8)])
+def test_bf16_wide_sharp_softmax(d, h):
+    """Wide kernel (d = 256 / 512, one-pass softmax with a lazy reference maximum) in the sharp
+    regime, where later key tiles raise a row's maximum by more than 2^8 and O is rescaled in TMEM."""
+    wl = ragged_workload("bf16", d=d, h=h, M=2, L_infer=0, wq_scale=8.0)
+    Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["bf16"])
+
+
 def test_rlb_and_batch_invariance_bit_exact():
     """P10/P18: a request's outputs are bit-identical alone or inside any batch."""
     wl = ragged_workload("bf16")
