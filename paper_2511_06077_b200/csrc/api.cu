@@ -838,7 +838,13 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
   const bool tc_attn = h->bf16 && stca::tc_available() && stca::tc_attention_supported(d);
   const bool tc_wide = h->bf16 && stca::tc_available() && stca::tc_attention_wide_supported(d);
-  const int qtile = tc_attn ? 128 : tc_wide ? 64 : 16;
+  // requests with at most 64 query rows (m_b h) take the transposed kernel (keys = MMA rows), which
+  // does not pad every request to a 128-row query tile; STCA_NO_NARROW=1 disables it (A/B runs)
+  int64_t max_req_rows = 0;
+  for (int64_t b = 0; b < B; ++b) max_req_rows = std::max<int64_t>(max_req_rows, (tgt_off[b + 1] - tgt_off[b]) * hh);
+  static const bool no_narrow = getenv("STCA_NO_NARROW") && atoi(getenv("STCA_NO_NARROW")) != 0;
+  const bool tc_narrow = tc_attn && !no_narrow && stca::tc_attention_narrow_supported(d, (int)std::min<int64_t>(max_req_rows, 1 << 30));
+  const int qtile = tc_narrow ? 64 : tc_attn ? 128 : tc_wide ? 64 : 16;
   std::vector<int64_t> it6;
   int64_t nit = stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, nullptr, 0);
   it6.resize((size_t)std::max<int64_t>(nit, 1) * 6);
@@ -882,7 +888,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   // item's prologue / epilogue), CTA c runs cta_items[cta_off[c] .. cta_off[c+1]) in LPT order
   int n_ctas = 0;
   std::vector<int32_t> ctal;  // cta_off [n_ctas + 1] | cta_items [nit]
-  if (tc_attn && nit > 0) {
+  if (tc_attn && !tc_narrow && nit > 0) {
     n_ctas = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit);
     std::vector<int64_t> cost((size_t)nit);
     for (int64_t i = 0; i < nit; ++i) cost[i] = (items[i].klen + 127) / 128 + 2;
@@ -918,7 +924,10 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
-    if (tc_attn) {
+    if (tc_narrow) {
+      CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, h->Y.p,
+                                   h->part.as<float>(), st));
+    } else if (tc_attn) {
       CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
                             h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
     } else if (tc_wide) {

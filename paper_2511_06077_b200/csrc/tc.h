@@ -59,6 +59,10 @@ cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, co
 cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
                     float *Cf, int64_t ldcf, cudaStream_t st);
 // d in {256, 512}: 64-row query tiles, M = 64 MMAs, two-pass softmax (tc_attn_wide.cu)
+// transposed ragged attention (keys as MMA rows) for requests with <= 64 query rows, d = 128
+bool tc_attention_narrow_supported(int d, int max_rows);
+cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
+                                int64_t n_items, void *Y, float *part, cudaStream_t st);
 bool tc_attention_wide_supported(int d);
 cudaError_t tc_attention_wide(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                               int64_t n_items, int d, void *Y, float *part, cudaStream_t st);

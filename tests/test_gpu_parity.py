@@ -34,12 +34,12 @@ def test_tiny_fp32():
 RAGGED = dict(lengths=np.array([1, 64, 200, 4097, 5000, 130, 9000]), m=[3, 0, 16, 64, 2, 33, 5])
 
 
-def ragged_workload(dtype, d=128, h=4, M=4, L_infer=4500, seed=1, ln_affine=True, wq_scale=1.0):
+def ragged_workload(dtype, d=128, h=4, M=4, L_infer=4500, seed=1, ln_affine=True, wq_scale=1.0, m=None):
     lengths = RAGGED["lengths"]
     cfg = make_cfg(B=len(lengths), d=d, h=h, M=M, dtype=dtype, L_infer=L_infer)
     wl = workload.make_workload(cfg, seed=seed, lengths=lengths, ln_affine=ln_affine, wq_scale=wq_scale)
     # ragged target counts (m_b = 0 allowed)
-    m = np.array(RAGGED["m"], dtype=np.int64)
+    m = np.array(RAGGED["m"] if m is None else m, dtype=np.int64)
     wl.tgt_off = np.concatenate([[0], np.cumsum(m)]).astype(np.int64)
     wl.xt = wl.xt[: wl.tgt_off[-1]] if wl.xt.shape[0] >= wl.tgt_off[-1] else np.resize(wl.xt, (wl.tgt_off[-1], d))
     rng = np.random.default_rng(seed + 100)
@@ -87,6 +87,19 @@ def test_bf16_wide_sharp_softmax(d, h):
     regime, where later key tiles raise a row's maximum by more than 2^8 and O is rescaled in TMEM."""
     wl = ragged_workload("bf16", d=d, h=h, M=2, L_infer=0, wq_scale=8.0)
     Z, z = run_gpu(wl)
+    check(wl, Z, z, TOL["bf16"])
+
+
+# at most 16 targets x 4 heads = 64 query rows per request: the transposed (keys = MMA rows) kernel
+NARROW_M = [3, 0, 16, 8, 2, 1, 5]
+
+
+@pytest.mark.parametrize("chunk_keys,wq_scale", [(0, 1.0), (1280, 1.0), (0, 8.0)])
+def test_bf16_narrow_requests(chunk_keys, wq_scale):
+    """Requests with m_b h <= 64 (tc_attn_narrow.cu): ragged lengths 1..9000, single- and multi-chunk
+    (partials + merge), and the sharp regime that triggers the lazy-maximum rescale of O^T."""
+    wl = ragged_workload("bf16", m=NARROW_M, wq_scale=wq_scale)
+    Z, z = run_gpu(wl, chunk_keys=chunk_keys)
     check(wl, Z, z, TOL["bf16"])
 
 
