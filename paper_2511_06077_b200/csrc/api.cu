@@ -838,13 +838,13 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
   const bool tc_attn = h->bf16 && stca::tc_available() && stca::tc_attention_supported(d);
   const bool tc_wide = h->bf16 && stca::tc_available() && stca::tc_attention_wide_supported(d);
-  // requests with at most 64 query rows (m_b h) take the transposed kernel (keys = MMA rows), which
-  // does not pad every request to a 128-row query tile; STCA_NO_NARROW=1 disables it (A/B runs)
-  int64_t max_req_rows = 0;
-  for (int64_t b = 0; b < B; ++b) max_req_rows = std::max<int64_t>(max_req_rows, (tgt_off[b + 1] - tgt_off[b]) * hh);
+  // A request with at most 64 query rows (m_b h) takes the transposed kernel (keys = MMA rows), which
+  // does not pad it to a 128-row query tile.  The choice is PER REQUEST (its items are moved behind
+  // the others and launched separately), so a request's arithmetic never depends on its batch
+  // (RLB invariance, P10).  STCA_NO_NARROW=1 disables it (A/B runs).
   static const bool no_narrow = getenv("STCA_NO_NARROW") && atoi(getenv("STCA_NO_NARROW")) != 0;
-  const bool tc_narrow = tc_attn && !no_narrow && stca::tc_attention_narrow_supported(d, (int)std::min<int64_t>(max_req_rows, 1 << 30));
-  const int qtile = tc_narrow ? 64 : tc_attn ? 128 : tc_wide ? 64 : 16;
+  const bool tc_narrow = tc_attn && !no_narrow;
+  const int qtile = tc_attn ? 128 : tc_wide ? 64 : 16;
   std::vector<int64_t> it6;
   int64_t nit = stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, nullptr, 0);
   it6.resize((size_t)std::max<int64_t>(nit, 1) * 6);
@@ -864,7 +864,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     max_rows = std::max<int>(max_rows, (int)rows);
     max_chunks = std::max<int>(max_chunks, (int)nc);
   }
-  std::vector<stca::AttnItem> items;
+  std::vector<stca::AttnItem> items, items_nar;
   items.reserve((size_t)nit);
   for (int64_t i = 0; i < nit; ++i) {
     const int64_t *o = &it6[6 * i];
@@ -873,8 +873,11 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
       const int32_t nc = stca_plan_chunks(h->len[b], (int32_t)h->chunk_cap, nullptr);
       if ((o[5] * G) / nc != grank) continue;
     }
-    items.emplace_back();
-    stca::AttnItem &a = items.back();
+    const bool nar = tc_narrow && stca::tc_attention_narrow_supported(d, (int)std::min<int64_t>(
+                                                                        (tgt_off[b + 1] - tgt_off[b]) * hh, 1 << 30));
+    std::vector<stca::AttnItem> &dst = nar ? items_nar : items;
+    dst.emplace_back();
+    stca::AttnItem &a = dst.back();
     a.qrow0 = o[1];
     a.nq = (int32_t)o[2];
     a.key0 = h->coff[b] + (o[3] - h->own0[b]);
@@ -883,17 +886,19 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     a.pad = 0;
     a.part_row = part_base[b] < 0 ? -1 : part_base[b] + o[5] * (tgt_off[b + 1] - tgt_off[b]) * hh + (o[1] - tgt_off[b] * hh);
   }
+  const int64_t nit_reg = (int64_t)items.size(), nit_nar = (int64_t)items_nar.size();
+  items.insert(items.end(), items_nar.begin(), items_nar.end());  // [128-row kernel items | narrow items]
   nit = (int64_t)items.size();
   // persistent d = 128 attention: LPT bins of work items over the SMs (cost = key tiles + 2 for the
   // item's prologue / epilogue), CTA c runs cta_items[cta_off[c] .. cta_off[c+1]) in LPT order
   int n_ctas = 0;
   std::vector<int32_t> ctal;  // cta_off [n_ctas + 1] | cta_items [nit]
-  if (tc_attn && !tc_narrow && nit > 0) {
-    n_ctas = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit);
-    std::vector<int64_t> cost((size_t)nit);
-    for (int64_t i = 0; i < nit; ++i) cost[i] = (items[i].klen + 127) / 128 + 2;
-    std::vector<int32_t> bin((size_t)nit);
-    stca_plan_persistent(cost.data(), nit, n_ctas, ctal_resize(ctal, n_ctas, nit), bin.data());
+  if (tc_attn && nit_reg > 0) {
+    n_ctas = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit_reg);
+    std::vector<int64_t> cost((size_t)nit_reg);
+    for (int64_t i = 0; i < nit_reg; ++i) cost[i] = (items[i].klen + 127) / 128 + 2;
+    std::vector<int32_t> bin((size_t)nit_reg);
+    stca_plan_persistent(cost.data(), nit_reg, n_ctas, ctal_resize(ctal, n_ctas, nit_reg), bin.data());
   }
   const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
   const size_t ctal_bytes = ctal.size() * sizeof(int32_t);
@@ -924,11 +929,12 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
-    if (tc_narrow) {
-      CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, h->Y.p,
-                                   h->part.as<float>(), st));
-    } else if (tc_attn) {
-      CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
+    if (tc_attn) {
+      if (nit_nar > 0)
+        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg, nit_nar, h->Y.p,
+                                     h->part.as<float>(), st));
+      if (nit_reg > 0)
+        CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
                             h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
     } else if (tc_wide) {
       CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
