@@ -900,6 +900,17 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     std::vector<int32_t> bin((size_t)nit_reg);
     stca_plan_persistent(cost.data(), nit_reg, n_ctas, ctal_resize(ctal, n_ctas, nit_reg), bin.data());
   }
+  // persistent narrow attention: its own LPT lists appended to ctal (indices relative to its items)
+  int n_ctas_nar = 0;
+  const size_t nar_at = ctal.size();
+  if (nit_nar > 0) {
+    n_ctas_nar = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit_nar);
+    std::vector<int64_t> cost((size_t)nit_nar);
+    for (int64_t i = 0; i < nit_nar; ++i) cost[i] = (items[nit_reg + i].klen + 127) / 128 + 2;
+    std::vector<int32_t> bin((size_t)nit_nar), v;
+    stca_plan_persistent(cost.data(), nit_nar, n_ctas_nar, ctal_resize(v, n_ctas_nar, nit_nar), bin.data());
+    ctal.insert(ctal.end(), v.begin(), v.end());
+  }
   const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
   const size_t ctal_bytes = ctal.size() * sizeof(int32_t);
   CU(h->items.ensure(items_bytes + 64));
@@ -931,8 +942,9 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     if (tc_attn) {
       if (nit_nar > 0)
-        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg, nit_nar, h->Y.p,
-                                     h->part.as<float>(), st));
+        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg,
+                                     h->ctal.as<int32_t>() + nar_at, h->ctal.as<int32_t>() + nar_at + n_ctas_nar + 1,
+                                     n_ctas_nar, h->Y.p, h->part.as<float>(), st));
       if (nit_reg > 0)
         CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
                             h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));

@@ -62,7 +62,8 @@ cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N
 // transposed ragged attention (keys as MMA rows) for requests with <= 64 query rows, d = 128
 bool tc_attention_narrow_supported(int d, int max_rows);
 cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
-                                int64_t n_items, void *Y, float *part, cudaStream_t st);
+                                const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
+                                cudaStream_t st);
 bool tc_attention_wide_supported(int d);
 cudaError_t tc_attention_wide(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                               int64_t n_items, int d, void *Y, float *part, cudaStream_t st);

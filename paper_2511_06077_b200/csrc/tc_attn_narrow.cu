@@ -9,7 +9,7 @@
 //   S^T [128 keys x 64 queries]  = X~_tile (SMEM, K-major A) . U^T (SMEM, K-major B)
 //   O^T [128 d    x 64 queries] += X~_tile^T (the SAME SMEM tile as an MN-major A) . P^T (SMEM, MN-major B)
 // so the MMA work per key tile is 128x64x128 twice (not 128x128x128 twice) and a CTA streams X~ at
-// HBM speed.  TMEM: S^T double buffer (2 x 64 columns) | O^T (64 columns).
+// HBM speed.  TMEM: S^T double buffer (2 x 64 columns) | O^T double buffer (2 x 64 columns).
 //
 // Softmax along TMEM lanes: a thread owns one key (lane) and 16 query columns (four warps per
 // lane quarter; with 8 warps of 32 columns the per-tile latency chain left the tile at ~2400 cycles).  A query's running maximum is LAZY (as in tc_attn_wide.cu): a key tile only triggers the
@@ -19,7 +19,7 @@
 // Sums stay per thread (per key, per query) until one reduction at the end.
 //
 // Warp roles (608 threads): 0..15 softmax (warp w: keys 32(w&3).., queries 16(w>>2)..) and output,
-// 16 TMA producer, 17 TMEM allocator + S issuer, 18 PV issuer.  One CTA per work item.
+// 16 TMA producer, 17 TMEM allocator + S issuer, 18 PV issuer.  Persistent: one CTA per SM.
 #include <math.h>
 
 #include "launch.h"
@@ -43,8 +43,8 @@ struct NCfg {
   static constexpr int U_BYTES = NQ * D * 2;           // U: 64 queries x 128 d, 2 boxes of 8 KB
   static constexpr int RED_BYTES = 4 * 4 * 16 * 4;     // [column group][quarter][16] column partials
   static constexpr int NSW = 16, THREADS = (NSW + 3) * 32;  // softmax warps; + producer, S / PV issuers
-  static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + U_BYTES + RED_BYTES + 64 + 256;
-  static constexpr uint32_t TS = 0, TO = 128;          // S^T buffers at 0 / 64, O^T at 128
+  static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + 2 * U_BYTES + RED_BYTES + 64 + 256;
+  static constexpr uint32_t TS = 0, TO = 128;          // S^T buffers at 0 / 64, O^T buffers at 128 / 192
 };
 
 // instruction descriptor with both operands MN-major (A = X~^T, B = P^T)
@@ -68,45 +68,52 @@ __device__ __forceinline__ float xreduce16(float (&v)[16], int lane) {
   return MAX ? fmaxf(v[0], o) : v[0] + o;
 }
 
+// PERSISTENT: CTA c runs items cta_items[cta_off[c] .. cta_off[c+1]) back to back (host LPT plan);
+// the X~ ring, the S / P double buffers and their barriers run across items, U (by TMA) and O^T are
+// double-buffered per item, so the next item's first tiles load and multiply while this item's
+// sums are reduced and its outputs written.
 __global__ void __launch_bounds__(NCfg::THREADS, 1)
-    k_tc_attention_narrow(const __grid_constant__ CUtensorMap mapX, const bf16 *__restrict__ U, int64_t NQ,
-                          const AttnItem *__restrict__ items, bf16 *__restrict__ Y, float *__restrict__ part) {
+    k_tc_attention_narrow(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapU,
+                          const AttnItem *__restrict__ items, const int32_t *__restrict__ cta_off,
+                          const int32_t *__restrict__ cta_items, bf16 *__restrict__ Y, float *__restrict__ part) {
   using C = NCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sX = smem;
   uint8_t *sP = sX + C::STAGES * C::X_BYTES;
-  uint8_t *sU = sP + 2 * C::P_BYTES;
-  float *sRed = reinterpret_cast<float *>(sU + C::U_BYTES);  // [4][4][16]
-  uint32_t *sFlag = reinterpret_cast<uint32_t *>(sRed + 4 * 4 * 16);  // [tile parity][column group]: 4 byte flags
+  uint8_t *sU = sP + 2 * C::P_BYTES;                                   // 2 buffers
+  float *sRed = reinterpret_cast<float *>(sU + 2 * C::U_BYTES);        // [4][4][16]
+  uint32_t *sFlag = reinterpret_cast<uint32_t *>(sRed + 4 * 4 * 16);   // [tile parity][column group]: 4 byte flags
   uint64_t *bar = reinterpret_cast<uint64_t *>(sFlag + 16);
-  uint64_t *u_full = bar;                      // NSW warp arrivals
-  uint64_t *x_full = bar + 1;                  // STAGES
+  uint64_t *u_full = bar;                      // 2 (TMA)
+  uint64_t *u_free = u_full + 2;               // 2 (S issuer commit after an item's last S)
+  uint64_t *x_full = u_free + 2;               // STAGES
   uint64_t *x_empty = x_full + C::STAGES;      // STAGES (PV commit)
   uint64_t *s_full = x_empty + C::STAGES;      // 2
   uint64_t *s_free = s_full + 2;               // 2 (NSW warps)
   uint64_t *p_full = s_free + 2;               // 2 (NSW warps)
   uint64_t *pv_done = p_full + 2;              // 2
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(pv_done + 2);
+  uint64_t *o_free = pv_done + 2;              // 2 (NSW warps: O^T buffer read out)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(o_free + 2);
 
-  pdl_wait();  // U comes from the preceding GEMM (programmatic dependent launch)
-  pdl_trigger();
-  const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nt = (it.klen + C::BK - 1) / C::BK;
+  const int i0 = cta_off[blockIdx.x], i1 = cta_off[blockIdx.x + 1];
 
   if (warp == C::NSW && lane == 0) {
     tma_prefetch(&mapX);
-    mbar_init(u_full, C::NSW);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);
-    }
+    tma_prefetch(&mapU);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&u_full[b], 1);
+      mbar_init(&u_free[b], 1);
       mbar_init(&s_full[b], 1);
       mbar_init(&s_free[b], C::NSW);
       mbar_init(&p_full[b], C::NSW);
       mbar_init(&pv_done[b], 1);
+      mbar_init(&o_free[b], C::NSW);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
     }
     fence_mbar_init();
   }
@@ -115,185 +122,203 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();  // U comes from the preceding GEMM (programmatic dependent launch)
+  pdl_trigger();
 
   if (warp == C::NSW) {
-    if (lane == 0) {  // ---------------- TMA producer: the item's key tiles ----------------
+    if (lane == 0) {  // ---------------- TMA producer: per item U, then its key tiles ----------------
       int s = 0, ph = 0;
-      for (int j = 0; j < nt; ++j) {
-        mbar_wait(&x_empty[s], ph ^ 1);
-        uint8_t *dst = sX + s * C::X_BYTES;
-        const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BK);
-        mbar_expect_tx(&x_full[s], C::X_BYTES);
-        tma_load_2d(dst, &mapX, &x_full[s], 0, row);
-        tma_load_2d(dst + C::X_BYTES / 2, &mapX, &x_full[s], 64, row);
-        if (++s == C::STAGES) { s = 0; ph ^= 1; }
+      for (int n = i0; n < i1; ++n) {
+        const AttnItem it = items[cta_items[n]];
+        const int ni = n - i0, ub = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
+        if (ni >= 2) mbar_wait(&u_free[ub], ((ni - 2) >> 1) & 1);
+        mbar_expect_tx(&u_full[ub], C::U_BYTES);
+        uint8_t *ud = sU + ub * C::U_BYTES;
+        tma_load_2d(ud, &mapU, &u_full[ub], 0, (int32_t)it.qrow0);  // rows past nq: finite, unused columns
+        tma_load_2d(ud + C::U_BYTES / 2, &mapU, &u_full[ub], 64, (int32_t)it.qrow0);
+        for (int j = 0; j < nt; ++j) {
+          mbar_wait(&x_empty[s], ph ^ 1);
+          uint8_t *dst = sX + s * C::X_BYTES;
+          const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BK);
+          mbar_expect_tx(&x_full[s], C::X_BYTES);
+          tma_load_2d(dst, &mapX, &x_full[s], 0, row);
+          tma_load_2d(dst + C::X_BYTES / 2, &mapX, &x_full[s], 64, row);
+          if (++s == C::STAGES) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == C::NSW + 1) {
     if (lane == 0) {  // ---------------- S issuer: S^T_j = X~_j U^T (SS, M = 128, N = 64) ----------------
       constexpr uint32_t idesc_s = idesc_bf16(128, C::NQ, 0);
-      const uint32_t aX = smem_u32(sX), aU = smem_u32(sU);
-      mbar_wait(u_full, 0);
-      int s = 0, ph = 0;
-      for (int j = 0; j < nt; ++j) {
-        const int b = j & 1;
-        mbar_wait(&x_full[s], ph);
-        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
-        tc_fence_after();
-        const uint32_t xs = aX + s * C::X_BYTES;
+      const uint32_t aX = smem_u32(sX);
+      int s = 0, ph = 0, g = 0;
+      for (int n = i0; n < i1; ++n) {
+        const AttnItem it = items[cta_items[n]];
+        const int ni = n - i0, ub = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
+        const uint32_t aU = smem_u32(sU + ub * C::U_BYTES);
+        mbar_wait(&u_full[ub], (ni >> 1) & 1);
+        for (int j = 0; j < nt; ++j, ++g) {
+          const int b = g & 1;
+          mbar_wait(&x_full[s], ph);
+          if (g >= 2) mbar_wait(&s_free[b], ((g - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t xs = aX + s * C::X_BYTES;
 #pragma unroll
-        for (int k = 0; k < C::D / 16; ++k)
-          umma_f16_ss(tmem + C::TS + b * C::NQ, sdesc_sw128(xs + (k >> 2) * (C::X_BYTES / 2) + (k & 3) * 32, 16, 1024),
-                      sdesc_sw128(aU + (k >> 2) * (C::U_BYTES / 2) + (k & 3) * 32, 16, 1024), idesc_s, k != 0);
-        umma_commit(&s_full[b]);
-        if (++s == C::STAGES) { s = 0; ph ^= 1; }
+          for (int k = 0; k < C::D / 16; ++k)
+            umma_f16_ss(tmem + C::TS + b * C::NQ, sdesc_sw128(xs + (k >> 2) * (C::X_BYTES / 2) + (k & 3) * 32, 16, 1024),
+                        sdesc_sw128(aU + (k >> 2) * (C::U_BYTES / 2) + (k & 3) * 32, 16, 1024), idesc_s, k != 0);
+          umma_commit(&s_full[b]);
+          if (++s == C::STAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit(&u_free[ub]);  // this item's U buffer may be reloaded
       }
     }
   } else if (warp == C::NSW + 2) {
     if (lane == 0) {  // ---------------- PV issuer: O^T += X~_j^T P_j^T (SS, both MN-major) ----------------
       constexpr uint32_t idesc_o = idesc_bf16_mn(128, C::NQ);
       const uint32_t aX = smem_u32(sX), aP = smem_u32(sP);
-      int s = 0;
-      for (int j = 0; j < nt; ++j) {
-        const int b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);  // P^T_j written (and O^T rescaled, if it had to be)
-        tc_fence_after();
-        const uint32_t xs = aX + s * C::X_BYTES, ps = aP + b * C::P_BYTES;
+      int s = 0, g = 0;
+      for (int n = i0; n < i1; ++n) {
+        const AttnItem it = items[cta_items[n]];
+        const int ni = n - i0, ob = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
+        if (ni >= 2) mbar_wait(&o_free[ob], ((ni - 2) >> 1) & 1);  // O^T buffer ob read out (item ni - 2)
+        for (int j = 0; j < nt; ++j, ++g) {
+          const int b = g & 1;
+          mbar_wait(&p_full[b], (g >> 1) & 1);  // P^T_j written (and O^T rescaled, if it had to be)
+          tc_fence_after();
+          const uint32_t xs = aX + s * C::X_BYTES, ps = aP + b * C::P_BYTES;
 #pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k)  // 16 keys per MMA: 2 swizzle atoms of 8 key rows
-          umma_f16_ss(tmem + C::TO, sdesc_sw128(xs + k * 2048, C::X_BYTES / 2, 1024),
-                      sdesc_sw128(ps + k * 2048, C::P_BYTES, 1024), idesc_o, (j | k) != 0);
-        umma_commit(&pv_done[b]);
-        umma_commit(&x_empty[s]);
-        if (++s == C::STAGES) s = 0;
+          for (int k = 0; k < C::BK / 16; ++k)  // 16 keys per MMA: 2 swizzle atoms of 8 key rows
+            umma_f16_ss(tmem + C::TO + ob * C::NQ, sdesc_sw128(xs + k * 2048, C::X_BYTES / 2, 1024),
+                        sdesc_sw128(ps + k * 2048, C::P_BYTES, 1024), idesc_o, (j | k) != 0);
+          umma_commit(&pv_done[b]);
+          umma_commit(&x_empty[s]);
+          if (++s == C::STAGES) s = 0;
+        }
       }
     }
   } else {  // ---------------- softmax warps 0..NSW-1 ----------------
     const int q = warp & 3, cg = warp >> 2;  // lane quarter (keys / d rows), 16-column query group
-    {  // U rows -> SMEM (SW128 K-major, 2 boxes of 64 d); rows >= nq are zero
-      for (int c = threadIdx.x; c < C::NQ * 16; c += C::NSW * 32) {
-        const int n = c >> 4, ch = c & 15;
-        const int64_t grow = it.qrow0 + n;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (n < it.nq && grow < NQ) v = *reinterpret_cast<const uint4 *>(U + grow * C::D + ch * 8);
-        *reinterpret_cast<uint4 *>(sU + (ch >> 3) * (C::U_BYTES / 2) + sw128_off(n, ch & 7)) = v;
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(u_full);
-    }
-    const int key = q * 32 + lane;                      // S^T lane = key within the tile; O^T lane = d
+    const int key = q * 32 + lane;           // S^T lane = key within the tile; O^T lane = d
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
-    float mref[16], l[16];
+    int g = 0;
+    for (int n = i0; n < i1; ++n) {
+      const AttnItem it = items[cta_items[n]];
+      const int ni = n - i0, ob = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
+      float mref[16], l[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      mref[c] = -INFINITY;
-      l[c] = 0.f;
-    }
-    for (int j = 0; j < nt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      for (int c = 0; c < 16; ++c) {
+        mref[c] = -INFINITY;
+        l[c] = 0.f;
+      }
+      for (int j = 0; j < nt; ++j, ++g) {
+        const int b = g & 1;
+        mbar_wait(&s_full[b], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[16];
+        tmem_ld16(tmem + lanes + C::TS + b * C::NQ + 16 * cg, sr);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[b]);
+        const bool kv = key < it.klen - j * C::BK;
+        float dm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 16; ++c) dm[c & 3] = fmaxf(dm[c & 3], __uint_as_float(sr[c]) - mref[c]);
+        const bool need = kv && fmaxf(fmaxf(dm[0], dm[1]), fmaxf(dm[2], dm[3])) > STCA_NARROW_LAZY;
+        const uint32_t wneed = __any_sync(0xffffffffu, need);
+        uint8_t *flags = reinterpret_cast<uint8_t *>(sFlag + 4 * b + cg);
+        if (lane == 0) flags[q] = (uint8_t)wneed;
+        named_bar_sync(1 + cg, 128);
+        if (*reinterpret_cast<volatile uint32_t *>(flags) != 0) {  // column maxima of this key tile (rare)
+          float v[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) v[c] = kv ? __uint_as_float(sr[c]) : -INFINITY;
+          const float red = xreduce16<true>(v, lane);
+          if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
+          named_bar_sync(1 + cg, 128);
+          float f[16];
+          bool any = false;
+#pragma unroll
+          for (int c = 0; c < 16; c += 4) {
+            float4 t = *reinterpret_cast<const float4 *>(sRed + (cg * 4) * 16 + c);
+#pragma unroll
+            for (int qq = 1; qq < 4; ++qq) {
+              const float4 u = *reinterpret_cast<const float4 *>(sRed + (cg * 4 + qq) * 16 + c);
+              t = make_float4(fmaxf(t.x, u.x), fmaxf(t.y, u.y), fmaxf(t.z, u.z), fmaxf(t.w, u.w));
+            }
+            const float tm[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const bool up = tm[e] > mref[c + e] + STCA_NARROW_LAZY;
+              f[c + e] = up ? ex2(mref[c + e] - tm[e]) : 1.f;  // 0 for the first maximum (-inf reference)
+              any |= up && j > 0;
+              if (up) mref[c + e] = tm[e];
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 16; ++c) l[c] *= f[c];
+          if (__any_sync(0xffffffffu, any)) {  // rescale O^T columns once the PVs issued so far are done
+            mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            tc_fence_after();
+            uint32_t o[16];
+            tmem_ld16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f[c]);
+            tmem_st16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);
+            tmem_st_wait();
+          }
+        }
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float p0 = kv ? ex2(__uint_as_float(sr[2 * i]) - mref[2 * i]) : 0.f;
+          const float p1 = kv ? ex2(__uint_as_float(sr[2 * i + 1]) - mref[2 * i + 1]) : 0.f;
+          l[2 * i] += p0;
+          l[2 * i + 1] += p1;
+          w[i] = pack_bf16(p0, p1);
+        }
+        if (g >= 2) mbar_wait(&pv_done[b], ((g - 2) >> 1) & 1);  // PV of tile g-2 has read P^T buffer b
+        uint8_t *prow = sP + b * C::P_BYTES;
+        *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b]);
+      }
+      // ---- sums over the keys: per warp by recursive halving, then the 4 lane quarters through SMEM ----
+      named_bar_sync(1 + cg, 128);  // the last tile's sRed reads are done
+      {
+        const float red = xreduce16<false>(l, lane);
+        if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
+      }
+      if (nt >= 1) mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);  // the item's last PV
+      tc_fence_before();
+      named_bar_sync(1 + cg, 128);
       tc_fence_after();
-      uint32_t sr[16];
-      tmem_ld16(tmem + lanes + C::TS + b * C::NQ + 16 * cg, sr);
+      uint32_t o[16];
+      tmem_ld16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);  // thread = output column d, 16 queries
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
-      const bool kv = key < it.klen - j * C::BK;
-      float dm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (lane == 0) mbar_arrive(&o_free[ob]);  // the PV issuer may start item ni + 2 in this buffer
+      const int d = key;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) dm[c & 3] = fmaxf(dm[c & 3], __uint_as_float(sr[c]) - mref[c]);
-      const bool need = kv && fmaxf(fmaxf(dm[0], dm[1]), fmaxf(dm[2], dm[3])) > STCA_NARROW_LAZY;
-      const uint32_t wneed = __any_sync(0xffffffffu, need);
-      uint8_t *flags = reinterpret_cast<uint8_t *>(sFlag + 4 * b + cg);
-      if (lane == 0) flags[q] = (uint8_t)wneed;
-      named_bar_sync(1 + cg, 128);
-      if (*reinterpret_cast<volatile uint32_t *>(flags) != 0) {  // column maxima of this key tile (rare)
-        float v[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = kv ? __uint_as_float(sr[c]) : -INFINITY;
-        const float red = xreduce16<true>(v, lane);
-        if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
-        named_bar_sync(1 + cg, 128);
-        float f[16];
-        bool any = false;
-#pragma unroll
-        for (int c = 0; c < 16; c += 4) {
-          float4 t = *reinterpret_cast<const float4 *>(sRed + (cg * 4) * 16 + c);
-#pragma unroll
-          for (int qq = 1; qq < 4; ++qq) {
-            const float4 u = *reinterpret_cast<const float4 *>(sRed + (cg * 4 + qq) * 16 + c);
-            t = make_float4(fmaxf(t.x, u.x), fmaxf(t.y, u.y), fmaxf(t.z, u.z), fmaxf(t.w, u.w));
+      for (int e = 0; e < 16; ++e) {
+        const int qn = 16 * cg + e;
+        if (qn < it.nq) {
+          const float ln = sRed[(cg * 4) * 16 + e] + sRed[(cg * 4 + 1) * 16 + e] + sRed[(cg * 4 + 2) * 16 + e] +
+                           sRed[(cg * 4 + 3) * 16 + e];
+          const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
+          if (it.part_row < 0) {
+            Y[(it.qrow0 + qn) * C::D + d] = y;
+          } else {  // partials hold the chunk's normalised output O / l, then (m, l)
+            uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
+            reinterpret_cast<bf16 *>(pr)[d] = y;
+            if (d == 0) *reinterpret_cast<float2 *>(pr + 2 * C::D) = make_float2(mref[e], ln);
           }
-          const float tm[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool up = tm[e] > mref[c + e] + STCA_NARROW_LAZY;
-            f[c + e] = up ? ex2(mref[c + e] - tm[e]) : 1.f;  // 0 for the first maximum (-inf reference)
-            any |= up && j > 0;
-            if (up) mref[c + e] = tm[e];
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) l[c] *= f[c];
-        if (__any_sync(0xffffffffu, any)) {  // rescale O^T columns once the PVs issued so far are done
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-          tc_fence_after();
-          uint32_t o[16];
-          tmem_ld16(tmem + lanes + C::TO + 16 * cg, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f[c]);
-          tmem_st16(tmem + lanes + C::TO + 16 * cg, o);
-          tmem_st_wait();
-        }
-      }
-      uint32_t w[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float p0 = kv ? ex2(__uint_as_float(sr[2 * i]) - mref[2 * i]) : 0.f;
-        const float p1 = kv ? ex2(__uint_as_float(sr[2 * i + 1]) - mref[2 * i + 1]) : 0.f;
-        l[2 * i] += p0;
-        l[2 * i + 1] += p1;
-        w[i] = pack_bf16(p0, p1);
-      }
-      if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // PV of tile j-2 has read P^T buffer b
-      uint8_t *prow = sP + b * C::P_BYTES;
-      *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg)) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
-      fence_proxy_async();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-    }
-    // ---- sums over the keys: per warp by recursive halving, then the 4 lane quarters through SMEM ----
-    named_bar_sync(1 + cg, 128);  // the last tile's sRed reads are done
-    {
-      const float red = xreduce16<false>(l, lane);
-      if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
-    }
-    if (nt >= 1) mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
-    tc_fence_before();
-    named_bar_sync(1 + cg, 128);
-    tc_fence_after();
-    uint32_t o[16];
-    tmem_ld16(tmem + lanes + C::TO + 16 * cg, o);  // thread = output column d = key, 16 query columns
-    tmem_ld_wait();
-    const int d = key;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int n = 16 * cg + e;
-      if (n < it.nq) {
-        const float ln = sRed[(cg * 4) * 16 + e] + sRed[(cg * 4 + 1) * 16 + e] + sRed[(cg * 4 + 2) * 16 + e] +
-                         sRed[(cg * 4 + 3) * 16 + e];
-        const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
-        if (it.part_row < 0) {
-          Y[(it.qrow0 + n) * C::D + d] = y;
-        } else {  // partials hold the chunk's normalised output O / l, then (m, l)
-          uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + n) * (int64_t)part_row_bytes(C::D, 2);
-          reinterpret_cast<bf16 *>(pr)[d] = y;
-          if (d == 0) *reinterpret_cast<float2 *>(pr + 2 * C::D) = make_float2(mref[e], ln);
         }
       }
     }
@@ -308,11 +333,13 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
 bool tc_attention_narrow_supported(int d, int max_rows) { return d == 128 && max_rows <= tc::NCfg::NQ; }
 
 cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
-                                int64_t n_items, void *Y, float *part, cudaStream_t st) {
+                                const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
+                                cudaStream_t st) {
   using C = tc::NCfg;
-  if (n_items <= 0) return cudaSuccess;
-  CUtensorMap mx;
-  if (!tc::make_map_bf16(&mx, Xt, T2, C::D, C::D, C::BK)) return cudaErrorInvalidValue;
+  if (n_ctas <= 0) return cudaSuccess;
+  CUtensorMap mx, mu;
+  if (!tc::make_map_bf16(&mx, Xt, T2, C::D, C::D, C::BK) || !tc::make_map_bf16(&mu, U, NQ, C::D, C::D, C::NQ))
+    return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc::k_tc_attention_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -320,8 +347,8 @@ cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64
     attr = true;
   }
   note_launch();
-  return launch_pdl(tc::k_tc_attention_narrow, dim3((unsigned)n_items), dim3(C::THREADS), (size_t)C::SMEM, st, mx,
-                    (const bf16 *)U, NQ, items, (bf16 *)Y, part);
+  return launch_pdl(tc::k_tc_attention_narrow, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx, mu,
+                    items, cta_off, cta_items, (bf16 *)Y, part);
 }
 
 }  // namespace stca
