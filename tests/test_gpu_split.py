@@ -37,17 +37,17 @@ def _run(m, wl, stream=None):
     return Z.cpu().numpy(), z.cpu().numpy()
 
 
-def split_workload():
-    cfg = make_cfg(B=3, m=64, dtype="bf16", L_infer=10000)
+def split_workload(m=64):
+    cfg = make_cfg(B=3, m=m, dtype="bf16", L_infer=10000)
     return workload.make_workload(cfg, seed=7, lengths=np.array([10000, 700, 3000]))
 
 
-@pytest.mark.parametrize("G", [2, 3, 8])
-def test_split_history_threads_bit_exact(G):
+@pytest.mark.parametrize("G,m", [(2, 64), (3, 64), (8, 64), (3, 8)])  # m = 8: 32 query rows, narrow kernel
+def test_split_history_threads_bit_exact(G, m):
     """G ranks as threads on one device (ThreadExchange) == the unsplit 1-GPU run, bit for bit."""
     import torch
     import paper_2511_06077_b200 as stca
-    wl = split_workload()
+    wl = split_workload(m)
     Z1, z1 = _run(_model(wl), wl)
     ex = stca.ThreadExchange(G)
     outs = [None] * G
