@@ -58,7 +58,7 @@ cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, co
 // C[M x N] = A[M x K] (bf16, lda) . B where Bt = B^T [N x K] bf16 K-major
 cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
                     float *Cf, int64_t ldcf, cudaStream_t st);
-// d in {256, 512}: 64-row query tiles, M = 64 MMAs, two-pass softmax (tc_attn_wide.cu)
+// d in {256, 512}: 64-row query tiles, M = 64 MMAs, one-pass softmax with a lazy maximum (tc_attn_wide.cu)
 // transposed ragged attention (keys as MMA rows) for requests with <= 64 query rows, d = 128
 bool tc_attention_narrow_supported(int d, int max_rows);
 cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
