@@ -169,6 +169,33 @@ void stca_plan_shards(const int64_t *cost, int64_t B, int32_t n_parts, int32_t *
  * [n_ctas + 1] offsets, then the item indices of each CTA in descending cost (ties by index). */
 void stca_plan_persistent(const int64_t *cost, int64_t n, int32_t n_ctas, int32_t *cta_list, int32_t *bin_out);
 
+/* ---- training data path into the ragged forward ----
+ * PAPER.md §3.3 "Subsequence selection" / "Batch-Level Load Balancing"; the
+ * algorithmic readings are DESIGN.md R-N2a (rounding) and R-N2b (allocation rule).  All pointers
+ * are DEVICE pointers owned by the caller; work is ordered on `stream` (NULL: legacy stream). */
+
+/* Per request b < B: L_train_b = 8 * floor((L_min + s_b (L_max - L_min)) / 8 + 1/2) (Eq. beta-scale
+ * P:L258 + P:L260, fp64; s_b ~ Beta(alpha, beta) drawn by the caller, in [0, 1]); the temporal suffix
+ * request req_b = min(L_train_b, n_b), n_b = hist_off[b+1] - hist_off[b]; the global length
+ * allocation alloc[b] <= req_b with sum(alloc) <= B * L_avg; new_off [B+1] = exclusive
+ * prefix sum of alloc, the ragged index over the compacted rows.
+ * Synchronises `stream` (reads a device status word).  INVALID_ARG for B outside [1, 49152],
+ * L_min > L_max, L_avg < 1, an s_b outside [0, 1] or an infeasible budget (sum of min(req_b, 8) >
+ * B * L_avg); alloc/new_off are then unspecified.  CUDA on a launch failure. */
+stca_status stca_rlb_allocate(const double *s, const int64_t *hist_off, int64_t B, int32_t L_min, int32_t L_max,
+                              int32_t L_avg, int64_t *alloc, int64_t *new_off, void *stream);
+
+/* Sequence compaction: the last alloc[b] rows of request b's history in X [T x row_bytes]
+ * (rows hist_off[b+1] - alloc[b] .. hist_off[b+1] - 1) are copied, back to back in request order, to
+ * P [new_off[B] x row_bytes], viewed as physical rows of L_avg tokens laid end to end.  The segment
+ * map: segs [n_seg x 3] int64 (row, start, len) triples, those of request b at seg_off[b] ..
+ * seg_off[b+1] - 1 (seg_off [B+1]); n_seg <= 2B when new_off[B] <= B * L_avg (capacity the caller
+ * provides).  alloc/new_off as written by stca_rlb_allocate.  row_bytes a positive multiple of 16, X
+ * and P 16-byte aligned, else INVALID_ARG.  Asynchronous (no host sync); rows are copied bit for bit. */
+stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const int64_t *hist_off, const int64_t *alloc,
+                             const int64_t *new_off, int64_t B, int32_t L_avg, void *P, int64_t *seg_off,
+                             int64_t *segs, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

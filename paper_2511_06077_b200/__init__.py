@@ -23,7 +23,8 @@ from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_ch
                    _Tensor, LIB_PATH)
 
 __all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_persistent", "plan_shards", "plan_split", "plan_suffix",
-           "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange"]
+           "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange", "rlb_allocate",
+           "rlb_compact"]
 
 
 def _ptr(x) -> int:
@@ -239,3 +240,35 @@ class ThreadExchange:
                 traceback.print_exc()
                 return 1
         return fn
+
+
+def rlb_allocate(s, hist_off, L_min: int, L_max: int, L_avg: int, stream=None):
+    """stca_rlb_allocate (include/stca.h): s float64 [B], hist_off int64 [B+1], CUDA tensors.
+    Returns (alloc int64 [B], new_off int64 [B+1]) as CUDA tensors."""
+    import torch
+    B = int(s.shape[0])
+    alloc = torch.empty(B, dtype=torch.int64, device=s.device)
+    new_off = torch.empty(B + 1, dtype=torch.int64, device=s.device)
+    st = lib().stca_rlb_allocate(_ptr(s), _ptr(hist_off), B, int(L_min), int(L_max), int(L_avg), _ptr(alloc),
+                                 _ptr(new_off), _stream(stream))
+    if st != 0:
+        raise StcaError(st, "stca_rlb_allocate")
+    return alloc, new_off
+
+
+def rlb_compact(X, hist_off, alloc, new_off, L_avg: int, P=None, stream=None):
+    """stca_rlb_compact (include/stca.h): X CUDA tensor [T x d] (any 2-D dtype, rows of a
+    multiple of 16 bytes).  Returns (P [B*L_avg x d] with rows < new_off[B] written, seg_off [B+1],
+    segs [2B x 3]) as CUDA tensors; the number of valid triples is seg_off[B]."""
+    import torch
+    B = int(alloc.shape[0])
+    if P is None:
+        P = torch.empty((B * int(L_avg), X.shape[1]), dtype=X.dtype, device=X.device)
+    seg_off = torch.empty(B + 1, dtype=torch.int64, device=X.device)
+    segs = torch.empty((2 * B, 3), dtype=torch.int64, device=X.device)
+    row_bytes = X.shape[1] * X.element_size()
+    st = lib().stca_rlb_compact(_ptr(X), row_bytes, _ptr(hist_off), _ptr(alloc), _ptr(new_off), B, int(L_avg),
+                                _ptr(P), _ptr(seg_off), _ptr(segs), _stream(stream))
+    if st != 0:
+        raise StcaError(st, "stca_rlb_compact")
+    return P, seg_off, segs

@@ -39,7 +39,7 @@ _I64P = ctypes.POINTER(ctypes.c_int64)
 SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy", "stca_last_error",
            "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
-           "stca_plan_split", "stca_plan_persistent", "stca_read_cache"]
+           "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact"]
 
 
 def lib():
@@ -83,6 +83,14 @@ def lib():
         L.stca_plan_persistent.argtypes = [_I64P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                            ctypes.POINTER(ctypes.c_int32)]
         L.stca_plan_persistent.restype = None
+        L.stca_rlb_allocate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p]
+        L.stca_rlb_allocate.restype = ctypes.c_int32
+        L.stca_rlb_compact.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.stca_rlb_compact.restype = ctypes.c_int32
         L.stca_read_cache.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                       ctypes.c_void_p]
         L.stca_read_cache.restype = ctypes.c_int

@@ -1,0 +1,219 @@
+// rlb_batch.cu -- the training data path into the ragged forward:
+// stochastic train lengths (Eq. beta-scale), temporal suffix, global length
+// allocation against the budget B * L_avg (reading R-N2b) and sequence
+// compaction with its segment map and ragged index.
+//
+// k_rlb_allocate: one CTA; B-sized integer work (reductions, O(B^2 / threads) ranking of the slack
+//   pass, scan).  Exact: int64 and unsigned __int128 for req_b * budget; the only floating-point
+//   decision (rounding L_raw to a multiple of 8) is taken in fp64 with explicit _rn ops, no FMA
+//   contraction, in the oracle's operation order.
+// k_rlb_segments: one CTA; (row, start, len) triples per sequence.
+// k_rlb_gather: the HBM-bound copy of the kept suffix rows into the physical rows (read + write
+//   of sum(alloc) * row_bytes); one 16-lane group per row, 16-byte vectors, grid = 8 x 148 CTAs.
+#include <stdint.h>
+
+#include "launch.h"
+#include "stca.h"
+
+namespace {
+
+__device__ int g_rlb_status;   // 0 ok, 1 infeasible budget, 2 s outside [0, 1]
+
+constexpr int kAllocThreads = 1024;
+constexpr int64_t kMaxB = 49152;   // 4 B of dynamic SMEM per sequence for the ranking
+
+// exclusive block scan of one value per thread; returns the prefix, *total = block sum
+__device__ int64_t block_exscan(int64_t v, int64_t *total) {
+  __shared__ int64_t warp_sum[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t s = lane < (int)(blockDim.x >> 5) ? warp_sum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sum[lane] = s;   // inclusive over warps
+  }
+  __syncthreads();
+  const int64_t before = (w ? warp_sum[w - 1] : 0) + x - v;
+  *total = warp_sum[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(kAllocThreads) k_rlb_allocate(const double *__restrict__ s,
+                                                                 const int64_t *__restrict__ hist_off, int64_t B,
+                                                                 int32_t L_min, int32_t L_max, int64_t budget,
+                                                                 int64_t *__restrict__ alloc,
+                                                                 int64_t *__restrict__ new_off) {
+  extern __shared__ int32_t trunc[];   // req_b - alloc_b if sequence b may take +8, else -1
+  __shared__ int64_t s_total, s_slack;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  // 1-2. L_train (Eq. beta-scale + rounding) and the temporal-suffix request; alloc <- req
+  int64_t part = 0;
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    const double sb = s[b];
+    if (!(sb >= 0.0 && sb <= 1.0)) s_bad = 2;
+    const double L_raw = __dadd_rn((double)L_min, __dmul_rn(sb, __dadd_rn((double)L_max, -(double)L_min)));
+    const int64_t L_train = 8 * (int64_t)floor(__dadd_rn(L_raw / 8.0, 0.5));
+    const int64_t n_b = hist_off[b + 1] - hist_off[b];
+    const int64_t req = L_train < n_b ? L_train : n_b;
+    alloc[b] = req;
+    part += req;
+  }
+  {
+    int64_t tot;
+    block_exscan(part, &tot);
+    if (threadIdx.x == 0) s_total = tot;
+  }
+  __syncthreads();
+  const int64_t total = s_total;
+  // 3. proportional scaling when over budget (exact), floor min(req, 8), one +8 per sequence
+  if (total > budget) {
+    part = 0;
+    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+      const int64_t req = alloc[b];
+      const unsigned __int128 num = (unsigned __int128)req * (unsigned __int128)budget;
+      int64_t a = 8 * (int64_t)(num / ((unsigned __int128)total * 8u));
+      const int64_t fl = req < 8 ? req : 8;
+      a = a > fl ? a : fl;
+      trunc[b] = (a + 8 <= req) ? (int32_t)(req - a) : -1;
+      alloc[b] = a;
+      part += a;
+    }
+    int64_t sum;
+    block_exscan(part, &sum);
+    if (threadIdx.x == 0) {
+      s_slack = budget - sum;
+      if (s_slack < 0) s_bad = 1;
+    }
+    __syncthreads();
+    const int64_t k = s_slack > 0 ? s_slack / 8 : 0;   // that many eligible sequences get +8
+    if (k > 0) {
+      for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+        const int32_t t = trunc[b];
+        if (t < 0) continue;
+        int64_t rank = 0;   // eligible sequences before b in (truncation desc, index asc)
+        for (int64_t c = 0; c < B && rank < k; ++c) {
+          const int32_t u = trunc[c];
+          rank += (u > t) || (u == t && c < b);
+        }
+        if (rank < k) alloc[b] += 8;
+      }
+      __syncthreads();
+    }
+  }
+  // ragged index over the compacted rows
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int64_t b = b0 + threadIdx.x;
+    const int64_t v = b < B ? alloc[b] : 0;
+    int64_t tot;
+    const int64_t ex = block_exscan(v, &tot);
+    if (b < B) new_off[b] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    new_off[B] = carry;
+    g_rlb_status = s_bad;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_rlb_segments(const int64_t *__restrict__ new_off, int64_t B, int32_t L_avg,
+                                                        int64_t *__restrict__ seg_off, int64_t *__restrict__ segs) {
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int64_t b = b0 + threadIdx.x;
+    int64_t p0 = 0, p1 = 0, cnt = 0;
+    if (b < B) {
+      p0 = new_off[b];
+      p1 = new_off[b + 1];
+      cnt = p1 > p0 ? (p1 - 1) / L_avg - p0 / L_avg + 1 : 0;
+    }
+    int64_t tot;
+    const int64_t ex = carry + block_exscan(cnt, &tot);
+    if (b < B) {
+      seg_off[b] = ex;
+      int64_t i = ex;
+      for (int64_t p = p0; p < p1; ++i) {
+        const int64_t row = p / L_avg, start = p - row * L_avg;
+        const int64_t n = (p1 - p) < (L_avg - start) ? (p1 - p) : (L_avg - start);
+        segs[3 * i + 0] = row;
+        segs[3 * i + 1] = start;
+        segs[3 * i + 2] = n;
+        p += n;
+      }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) seg_off[B] = carry;
+}
+
+constexpr int kGroup = 16;   // lanes per physical row
+constexpr int kGatherThreads = 256;
+
+__global__ void __launch_bounds__(kGatherThreads) k_rlb_gather(const uint4 *__restrict__ X,
+                                                                const int64_t *__restrict__ hist_off,
+                                                                const int64_t *__restrict__ alloc,
+                                                                const int64_t *__restrict__ new_off, int64_t B,
+                                                                int64_t cpr, uint4 *__restrict__ P) {
+  const int64_t total = new_off[B];
+  const int g = threadIdx.x % kGroup;
+  const int64_t groups = (int64_t)gridDim.x * (kGatherThreads / kGroup);
+  for (int64_t p = (int64_t)blockIdx.x * (kGatherThreads / kGroup) + threadIdx.x / kGroup; p < total; p += groups) {
+    int64_t lo = 0, hi = B - 1;   // last b with new_off[b] <= p
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(new_off + mid) <= p) lo = mid; else hi = mid - 1;
+    }
+    const int64_t src = __ldg(hist_off + lo + 1) - __ldg(alloc + lo) + (p - __ldg(new_off + lo));
+    const uint4 *in = X + src * cpr;
+    uint4 *out = P + p * cpr;
+    for (int64_t c = g; c < cpr; c += kGroup) __stcs(out + c, __ldcs(in + c));
+  }
+}
+
+}  // namespace
+
+extern "C" stca_status stca_rlb_allocate(const double *s, const int64_t *hist_off, int64_t B, int32_t L_min,
+                                         int32_t L_max, int32_t L_avg, int64_t *alloc, int64_t *new_off,
+                                         void *stream) {
+  if (B < 1 || B > kMaxB || L_min < 0 || L_max < L_min || L_avg < 1 || !s || !hist_off || !alloc || !new_off)
+    return STCA_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = (size_t)B * sizeof(int32_t);
+  if (cudaFuncSetAttribute(k_rlb_allocate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return STCA_ERR_CUDA;
+  k_rlb_allocate<<<1, kAllocThreads, smem, st>>>(s, hist_off, B, L_min, L_max, (int64_t)B * L_avg, alloc, new_off);
+  stca::note_launch();
+  int status = 0;
+  if (cudaMemcpyFromSymbolAsync(&status, g_rlb_status, sizeof(int), 0, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return STCA_ERR_CUDA;
+  return status ? STCA_ERR_INVALID_ARG : STCA_OK;
+}
+
+extern "C" stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const int64_t *hist_off,
+                                        const int64_t *alloc, const int64_t *new_off, int64_t B, int32_t L_avg,
+                                        void *P, int64_t *seg_off, int64_t *segs, void *stream) {
+  if (B < 1 || L_avg < 1 || row_bytes < 16 || row_bytes % 16 || !X || !hist_off || !alloc || !new_off || !P ||
+      !seg_off || !segs || ((uintptr_t)X | (uintptr_t)P) % 16)
+    return STCA_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_rlb_segments<<<1, 1024, 0, st>>>(new_off, B, L_avg, seg_off, segs);
+  k_rlb_gather<<<8 * 148, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, row_bytes / 16,
+                                                   (uint4 *)P);
+  stca::note_launch(2);
+  return cudaGetLastError() == cudaSuccess ? STCA_OK : STCA_ERR_CUDA;
+}
