@@ -9,7 +9,8 @@
 //   contraction, in the oracle's operation order.
 // k_rlb_segments: one CTA; (row, start, len) triples per sequence.
 // k_rlb_gather: the HBM-bound copy of the kept suffix rows into the physical rows (read + write
-//   of sum(alloc) * row_bytes); one 16-lane group per row, 16-byte vectors, grid = 8 x 148 CTAs.
+//   of sum(alloc) * row_bytes); one warp per 4-KB range of P, 8 x 16-B streaming loads in flight per
+//   lane, grid = 8 x 148 CTAs of 8 warps.
 #include <stdint.h>
 
 #include "launch.h"
@@ -160,27 +161,51 @@ __global__ void __launch_bounds__(1024) k_rlb_segments(const int64_t *__restrict
   if (threadIdx.x == 0) seg_off[B] = carry;
 }
 
-constexpr int kGroup = 16;   // lanes per physical row
+constexpr int kUnroll = 8;   // 16-B chunks in flight per lane
 constexpr int kGatherThreads = 256;
 
+// Each warp copies a contiguous range of 32 x kUnroll 16-B chunks of P (4 KB); lane l takes chunks
+// l, l + 32, ...  A lane finds the sequence of its first chunk by binary search in new_off and walks
+// forward for the rest (rows only increase), then issues all kUnroll loads before any store.
 __global__ void __launch_bounds__(kGatherThreads) k_rlb_gather(const uint4 *__restrict__ X,
                                                                 const int64_t *__restrict__ hist_off,
                                                                 const int64_t *__restrict__ alloc,
                                                                 const int64_t *__restrict__ new_off, int64_t B,
                                                                 int64_t cpr, uint4 *__restrict__ P) {
-  const int64_t total = new_off[B];
-  const int g = threadIdx.x % kGroup;
-  const int64_t groups = (int64_t)gridDim.x * (kGatherThreads / kGroup);
-  for (int64_t p = (int64_t)blockIdx.x * (kGatherThreads / kGroup) + threadIdx.x / kGroup; p < total; p += groups) {
+  const int64_t total = new_off[B] * cpr;   // chunks to write
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kGatherThreads / 32);
+  constexpr int64_t kRange = 32 * kUnroll;
+  for (int64_t c0 = ((int64_t)blockIdx.x * (kGatherThreads / 32) + (threadIdx.x >> 5)) * kRange; c0 < total;
+       c0 += warps * kRange) {
+    int64_t c = c0 + lane;
+    if (c >= total) continue;
+    int64_t p = c / cpr;
     int64_t lo = 0, hi = B - 1;   // last b with new_off[b] <= p
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
       if (__ldg(new_off + mid) <= p) lo = mid; else hi = mid - 1;
     }
-    const int64_t src = __ldg(hist_off + lo + 1) - __ldg(alloc + lo) + (p - __ldg(new_off + lo));
-    const uint4 *in = X + src * cpr;
-    uint4 *out = P + p * cpr;
-    for (int64_t c = g; c < cpr; c += kGroup) __stcs(out + c, __ldcs(in + c));
+    int64_t b = lo, nb = __ldg(new_off + b + 1), shift = (__ldg(hist_off + b + 1) - __ldg(alloc + b)) - __ldg(new_off + b);
+    uint4 v[kUnroll];
+    int64_t dst[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      c = c0 + lane + 32 * u;
+      dst[u] = c < total ? c : -1;
+      if (c < total) {
+        p = c / cpr;
+        while (nb <= p) {   // next sequence (empty ones are skipped)
+          ++b;
+          nb = __ldg(new_off + b + 1);
+          shift = (__ldg(hist_off + b + 1) - __ldg(alloc + b)) - __ldg(new_off + b);
+        }
+        v[u] = __ldcs(X + (p + shift) * cpr + (c - p * cpr));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (dst[u] >= 0) __stcs(P + dst[u], v[u]);
   }
 }
 
