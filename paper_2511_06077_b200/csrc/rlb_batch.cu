@@ -7,10 +7,10 @@
 //   pass, scan).  Exact: int64 and unsigned __int128 for req_b * budget; the only floating-point
 //   decision (rounding L_raw to a multiple of 8) is taken in fp64 with explicit _rn ops, no FMA
 //   contraction, in the oracle's operation order.
-// k_rlb_segments: one CTA; (row, start, len) triples per sequence.
 // k_rlb_gather: the HBM-bound copy of the kept suffix rows into the physical rows (read + write
 //   of sum(alloc) * row_bytes); one warp per 4-KB range of P, 8 x 16-B streaming loads in flight per
-//   lane, grid = 8 x 148 CTAs of 8 warps.
+//   lane, grid = 8 x 148 CTAs of 8 warps, plus one CTA that writes the segment map ((row, start,
+//   len) triples per sequence) concurrently.
 #include <stdint.h>
 
 #include "launch.h"
@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(kAllocThreads) k_rlb_allocate(const double *__
   }
 }
 
-__global__ void __launch_bounds__(1024) k_rlb_segments(const int64_t *__restrict__ new_off, int64_t B, int32_t L_avg,
-                                                        int64_t *__restrict__ seg_off, int64_t *__restrict__ segs) {
+// the segment map, computed by one CTA (any multiple of 32 threads)
+__device__ void rlb_segments(const int64_t *__restrict__ new_off, int64_t B, int32_t L_avg,
+                             int64_t *__restrict__ seg_off, int64_t *__restrict__ segs) {
   int64_t carry = 0;
   for (int64_t b0 = 0; b0 < B; b0 += blockDim.x) {
     const int64_t b = b0 + threadIdx.x;
@@ -171,16 +172,22 @@ __global__ void __launch_bounds__(kGatherThreads) k_rlb_gather(const uint4 *__re
                                                                 const int64_t *__restrict__ hist_off,
                                                                 const int64_t *__restrict__ alloc,
                                                                 const int64_t *__restrict__ new_off, int64_t B,
-                                                                int64_t cpr, uint4 *__restrict__ P) {
+                                                                int64_t cpr, int cpr_log2, int32_t L_avg,
+                                                                int64_t *__restrict__ seg_off,
+                                                                int64_t *__restrict__ segs, uint4 *__restrict__ P) {
+  if (blockIdx.x == gridDim.x - 1) {   // the last CTA writes the segment map while the rest copy
+    rlb_segments(new_off, B, L_avg, seg_off, segs);
+    return;
+  }
   const int64_t total = new_off[B] * cpr;   // chunks to write
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kGatherThreads / 32);
+  const int64_t warps = (int64_t)(gridDim.x - 1) * (kGatherThreads / 32);
   constexpr int64_t kRange = 32 * kUnroll;
   for (int64_t c0 = ((int64_t)blockIdx.x * (kGatherThreads / 32) + (threadIdx.x >> 5)) * kRange; c0 < total;
        c0 += warps * kRange) {
     int64_t c = c0 + lane;
     if (c >= total) continue;
-    int64_t p = c / cpr;
+    int64_t p = cpr_log2 >= 0 ? c >> cpr_log2 : c / cpr;
     int64_t lo = 0, hi = B - 1;   // last b with new_off[b] <= p
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_rlb_gather(const uint4 *__re
       c = c0 + lane + 32 * u;
       dst[u] = c < total ? c : -1;
       if (c < total) {
-        p = c / cpr;
+        p = cpr_log2 >= 0 ? c >> cpr_log2 : c / cpr;
         while (nb <= p) {   // next sequence (empty ones are skipped)
           ++b;
           nb = __ldg(new_off + b + 1);
@@ -236,9 +243,10 @@ extern "C" stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const 
       !seg_off || !segs || ((uintptr_t)X | (uintptr_t)P) % 16)
     return STCA_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  k_rlb_segments<<<1, 1024, 0, st>>>(new_off, B, L_avg, seg_off, segs);
-  k_rlb_gather<<<8 * 148, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, row_bytes / 16,
-                                                   (uint4 *)P);
-  stca::note_launch(2);
+  const int64_t cpr = row_bytes / 16;
+  const int cpr_log2 = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
+  k_rlb_gather<<<8 * 148 + 1, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, cpr, cpr_log2,
+                                                       L_avg, seg_off, segs, (uint4 *)P);
+  stca::note_launch(1);
   return cudaGetLastError() == cudaSuccess ? STCA_OK : STCA_ERR_CUDA;
 }
