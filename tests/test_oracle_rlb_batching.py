@@ -73,7 +73,7 @@ def test_allocate_budget_invariants_seeded_sweep():
         try:
             a = rb.allocate(req, budget)
         except rb.InfeasibleBudget:
-            assert sum(min(int(v), 8) for v in req) <= budget or True
+            assert req.sum() > budget            # only an over-budget batch can be infeasible
             continue
         assert a.sum() <= budget                                         # hard bound
         assert np.all(a <= req) and np.all(a >= np.minimum(req, 8))
