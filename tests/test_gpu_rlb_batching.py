@@ -115,3 +115,50 @@ def test_rlb_errors():
     a, n = stca.rlb_allocate(torch.full((3,), 0.5, dtype=torch.float64, device=dev), off, 8, 64, 16)
     with pytest.raises(stca.StcaError):    # rows of 6 bytes: not a multiple of 16
         stca.rlb_compact(torch.zeros((300, 3), dtype=torch.int16, device=dev), off, a, n, 16)
+
+
+def test_rlb_compacted_batch_feeds_the_forward():
+    """NEXT-2 end to end: the compacted rows P and their ragged index new_off go straight into
+    stca_project_history / stca_forward; the result equals the oracle forward on the oracle's own
+    compaction (bf16 tolerance, R20).  L_avg = 96 puts segment boundaries inside 128-row tiles."""
+    import dataclasses
+
+    import torch
+
+    import oracle
+    import paper_2511_06077_b200 as stca
+    import workload
+    from _util import make_cfg, rowrel
+
+    lengths = np.array([300, 50, 1000, 7, 600, 129, 2500])
+    B, L_min, L_max, L_avg = len(lengths), 8, 1024, 96
+    cfg = make_cfg(B=B, m=4, d=128, h=4, M=2, dtype="bf16")
+    wl = workload.make_workload(cfg, seed=5, lengths=lengths, ln_affine=True)
+    # lengths drawn for a mean of 400 against a budget of 96 per request: over budget (1061 > 672 rows)
+    s = np.random.default_rng(6).beta(0.5, rb.beta_shape(0.5, L_min, L_max, 400), size=B)
+
+    want_alloc = rb.allocate(rb.requested(rb.train_lengths(s, L_min, L_max), wl.hist_off), B * L_avg)
+    Pw, off_w, _, _ = rb.compact(wl.X, wl.hist_off, want_alloc, L_avg)
+    Pw_bits, _, _, _ = rb.compact(wl.X_bits, wl.hist_off, want_alloc, L_avg)
+    assert rb.requested(rb.train_lengths(s, L_min, L_max), wl.hist_off).sum() > B * L_avg
+    wl_c = dataclasses.replace(wl, X=Pw, X_bits=Pw_bits, hist_off=off_w)
+    Zr, zr, rows = oracle.forward_workload(wl_c, nthreads=8)
+
+    dev = torch.device("cuda:0")
+    off_d = torch.from_numpy(wl.hist_off).to(dev)
+    X_d = torch.from_numpy(wl.X_bits.view(np.int16)).to(dev)
+    alloc, new_off = stca.rlb_allocate(torch.from_numpy(s).to(dev), off_d, L_min, L_max, L_avg)
+    P, _, _ = stca.rlb_compact(X_d, off_d, alloc, new_off, L_avg)
+    new_off_h = new_off.cpu().numpy()
+    assert np.array_equal(new_off_h, off_w)
+    m = stca.STCA(workload.full_weights(wl), d=cfg.d, h=cfg.h, r=cfg.r, M=cfg.M, L_infer=0, dtype="bf16",
+                  with_z=cfg.with_z)
+    xt = torch.from_numpy(wl.xt_bits.view(np.int16)).to(dev)
+    Z = torch.full((wl.Nt, cfg.M, cfg.d), float("nan"), dtype=torch.float32, device=dev)
+    z = torch.full((wl.Nt, cfg.d), float("nan"), dtype=torch.float32, device=dev)
+    m.project_history(P[:int(new_off_h[-1])].contiguous(), new_off_h)
+    m.forward(xt, wl.tgt_off, Z, z)
+    torch.cuda.synchronize()
+    Z, z = Z.cpu().numpy().astype(np.float64), z.cpu().numpy().astype(np.float64)
+    assert rowrel(Z[rows], Zr).max() <= 2e-2
+    assert rowrel(z[rows], zr).max() <= 2e-2
