@@ -9,7 +9,7 @@
 //   contraction, in the oracle's operation order.
 // k_rlb_gather: the HBM-bound copy of the kept suffix rows into the physical rows (read + write
 //   of sum(alloc) * row_bytes); one warp per 4-KB range of P, 8 x 16-B streaming loads in flight per
-//   lane, grid = 8 x 148 CTAs of 8 warps, plus one CTA that writes the segment map ((row, start,
+//   lane, grid = 4 x 148 CTAs of 8 warps (all resident: <= 64 registers), plus one CTA that writes the segment map ((row, start,
 //   len) triples per sequence) concurrently.
 #include <stdint.h>
 
@@ -168,7 +168,7 @@ constexpr int kGatherThreads = 256;
 // Each warp copies a contiguous range of 32 x kUnroll 16-B chunks of P (4 KB); lane l takes chunks
 // l, l + 32, ...  A lane finds the sequence of its first chunk by binary search in new_off and walks
 // forward for the rest (rows only increase), then issues all kUnroll loads before any store.
-__global__ void __launch_bounds__(kGatherThreads) k_rlb_gather(const uint4 *__restrict__ X,
+__global__ void __launch_bounds__(kGatherThreads, 4) k_rlb_gather(const uint4 *__restrict__ X,
                                                                 const int64_t *__restrict__ hist_off,
                                                                 const int64_t *__restrict__ alloc,
                                                                 const int64_t *__restrict__ new_off, int64_t B,
@@ -245,7 +245,7 @@ extern "C" stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const 
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t cpr = row_bytes / 16;
   const int cpr_log2 = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
-  k_rlb_gather<<<8 * 148 + 1, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, cpr, cpr_log2,
+  k_rlb_gather<<<4 * 148 + 1, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, cpr, cpr_log2,
                                                        L_avg, seg_off, segs, (uint4 *)P);
   stca::note_launch(1);
   return cudaGetLastError() == cudaSuccess ? STCA_OK : STCA_ERR_CUDA;
