@@ -7,15 +7,25 @@ A step = one pass of the whole hot path over one batc
 stca_project_history (suffix truncation + X~(i) for every layer) then stca_forward
 (q(1), M x [U, ragged attention, o(i), fusion], z).  Inputs are resident in HBM when
 the timed region starts; X (655 MB at serve) and the X~ cache (2.6 GB) are larger
-than the 126 MB L2, so no flush is needed between steps.  Multi-GPU is weak scaling:
-every rank runs its own seeded serve-shaped shard, with no collective on the data
-path; the time is the max over ranks.  The JSON line carries the roofline of the
-dominant kernel (the history projection), the oracle's CPU baseline, the end-to-end
-number through the C ABI with host buffers, the launch count and the SM clocks.
+than the 126 MB L2, so no flush is needed between steps.
+
+Multi-GPU is STRONG scaling: every rank draws the same
+global request set (seed), partitions it with the library's LPT planner
+(stca_plan_shards over the cost c_b = L'_b 6rd^2M + m_b L'_b 4hdM + m_b c_tgt) and
+runs its own requests; there is no collective on the data path.  value = the global
+N_t / the max over ranks of the device time of a step.  `--config split1` runs the
+split-history path (one 10k history over all ranks, one all-gather per layer).
+
+The JSON line carries the roofline of the projection AND of the attention kernel
+(per-phase CUDA events recorded by the library on the launching stream, in a
+separate profiled pass after the timed one), the oracle's CPU baseline, the
+end-to-end number through the C ABI with host buffers, the launch count and the
+SM clocks sampled during the timed region.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -44,17 +54,42 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
 
 
+# ---------------------------------------------------------------------------
+# request sharding (PAR1): LPT over the per-request cost of SURVEY §8(e)
+# ---------------------------------------------------------------------------
+def request_cost(wl) -> np.ndarray:
+    """c_b = L'_b (6 r d^2 M) + m_b L'_b (4 h d M) + m_b c_tgt, c_tgt = sum_i (6r + 8 + 2(i+1)) d^2
+    (FLOPs: history projection, attention, target side; exact int64)."""
+    c = wl.cfg
+    L = np.minimum(wl.lengths, c.L_infer) if c.L_infer else wl.lengths.copy()
+    m = np.diff(wl.tgt_off)
+    c_tgt = sum((6 * c.r + 8 + 2 * (i + 1)) * c.d * c.d for i in range(1, c.M + 1))
+    return (L * (6 * c.r * c.d * c.d * c.M) + m * L * (4 * c.h * c.d * c.M) + m * c_tgt).astype(np.int64)
+
+
+def shard_requests(wl, world: int, rank: int) -> np.ndarray:
+    """The requests rank `rank` of `world` owns, in generation order (stca_plan_shards, identical on
+    every rank: integer costs, ties to the lowest index)."""
+    if world <= 1:
+        return np.arange(len(wl.lengths), dtype=np.int64)
+    from paper_2511_06077_b200 import _lib
+    part = _lib.plan_shards(request_cost(wl), world)
+    return np.nonzero(part == rank)[0].astype(np.int64)
+
+
 def algorithmic(wl):
-    """Algorithmic work per step (DESIGN.md §Roofline): FLOPs / bytes of the method itself."""
+    """Algorithmic work per step (DESIGN.md §6): FLOPs / bytes of the method itself."""
     c = wl.cfg
     L = np.minimum(wl.lengths, c.L_infer) if c.L_infer else wl.lengths
     T2 = int(L.sum())
     m = np.diff(wl.tgt_off)
     proj_flops = 6.0 * c.r * c.d * c.d * T2 * c.M                      # 3 GEMMs of d x rd per token per layer
     proj_bytes = 2.0 * c.d * T2 + 2.0 * c.d * T2 * c.M                # read X once, write M layers (bf16)
-    attn_flops = float(np.sum(4.0 * m * c.h * c.d * L)) * c.M          # S = U X~^T and Y = P X~
-    attn_bytes = float(np.sum(2.0 * c.d * L + 6.0 * m * c.d)) * c.M
-    return dict(T2=T2, proj_flops=proj_flops, proj_bytes=proj_bytes, attn_flops=attn_flops, attn_bytes=attn_bytes)
+    # attention, PER LAYER (one a4 launch): S = U X~^T and Y = P X~; bytes = X~ once + q in / o out (fused minimum)
+    attn_flops = float(np.sum(4.0 * m * c.h * c.d * L))
+    attn_bytes = float(np.sum(2.0 * c.d * L + 6.0 * m * c.d))
+    return dict(T2=T2, proj_flops=proj_flops, proj_bytes=proj_bytes, attn_flops_layer=attn_flops,
+                attn_bytes_layer=attn_bytes)
 
 
 class Clocks:
@@ -106,18 +141,18 @@ class Clocks:
                 "source": "NVML, 10 ms, during the timed region"}
 
 
-def oracle_sample(wl, budget_s=20.0, reps=1):
+def oracle_sample(wl, budget_s=20.0):
     """cpu_baseline: the oracle as it stands, threads over requests on the host cores, on a
     bounded deterministic sample (the first k requests, k = cores)."""
     import oracle
     cores = os.cpu_count() or 1
     k = min(cores, len(wl.lengths))
     reqs = list(range(k))
+    sub = workload.subset(wl, reqs)
     t0 = time.perf_counter()
-    for _ in range(reps):
-        oracle.forward_workload(wl, requests=reqs, nthreads=cores)
-    dt = (time.perf_counter() - t0) / reps
-    targets = int(sum(wl.tgt_off[b + 1] - wl.tgt_off[b] for b in reqs))
+    oracle.forward_workload(sub, nthreads=cores)
+    dt = time.perf_counter() - t0
+    targets = sub.Nt
     return {"value": targets / dt, "unit": UNIT, "cores": min(cores, k), "kind": "oracle",
             "sample": f"first {k} of {len(wl.lengths)} requests ({targets} targets, full history each), "
                       f"{dt:.2f} s per pass"}
@@ -125,23 +160,21 @@ def oracle_sample(wl, budget_s=20.0, reps=1):
 
 def run_reference(args, wl):
     """--impl reference: the f64 oracle timed as the reference arm on host cores."""
-    import oracle  # noqa: F401
+    import oracle as orc
     cores = os.cpu_count() or 1
     k = min(cores, len(wl.lengths))
-    reqs = list(range(k))
-    import oracle as orc
+    sub = workload.subset(wl, list(range(k)))
     for _ in range(args.warmup):
-        orc.forward_workload(wl, requests=reqs, nthreads=cores)
+        orc.forward_workload(sub, nthreads=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        orc.forward_workload(wl, requests=reqs, nthreads=cores)
+        orc.forward_workload(sub, nthreads=cores)
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    targets = int(sum(wl.tgt_off[b + 1] - wl.tgt_off[b] for b in reqs))
+    targets = sub.Nt
     v = targets / dt
-    c = wl.cfg
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(wl, args),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": min(cores, k), "kind": "oracle",
                              "sample": f"each step: first {k} of {len(wl.lengths)} requests ({targets} targets)"},
@@ -156,8 +189,49 @@ def config_dict(wl, args):
             "L_avg": float(L.mean()), "L_max": int(L.max()), "L_infer": c.L_infer, "d": c.d, "h": c.h, "r": c.r,
             "M": c.M, "T": wl.T, "N_t": wl.Nt,
             "parallelism": (f"split-history over {args.gpus} GPU(s) (NCCL all-gather of partials per layer)"
-                            if c.name == "split1" else f"requests sharded over {args.gpus} GPU(s), weak"),
+                            if c.name == "split1" else
+                            f"one global request set, LPT-sharded over {args.gpus} GPU(s) (stca_plan_shards), "
+                            "no collective on the data path"),
             "l2": "inputs larger than L2 (X and the X~ cache exceed 126 MB); no flush", "seed": args.seed}
+
+
+def lib_sha256():
+    from paper_2511_06077_b200 import _lib
+    h = hashlib.sha256()
+    with open(_lib.LIB_PATH, "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
+def traffic_for(config, kernel):
+    """ncu DRAM bytes per launch for `kernel` at `config`, from profiles/traffic_r2.json -- only if that
+    capture was taken of THIS library build (sha256), else None."""
+    tf = os.path.join(ROOT, "profiles", "traffic_r2.json")
+    try:
+        t = json.load(open(tf)).get(config, {}).get(kernel)
+        if t and t.get("lib_sha256") == lib_sha256():
+            return t.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+def roofline_entry(name, kernel, flops, bytes_, ms, pk, peak_kind, config):
+    """Bound by intensity against the ridge of the peaks in use; achieved = algorithmic work per launch
+    / event-timed launch duration."""
+    tf_peak = pk["bf16_tflops"] if peak_kind == "burst" else pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    bw_peak = pk["hbm_gbs"]
+    ridge = tf_peak * 1e12 / (bw_peak * 1e9)
+    intensity = flops / bytes_ if bytes_ else float("inf")
+    if intensity >= ridge:
+        achieved, peak, unit, bound = flops / (ms * 1e-3) / 1e12, tf_peak, "TFLOP/s", "tensor"
+    else:
+        achieved, peak, unit, bound = bytes_ / (ms * 1e-3) / 1e9, bw_peak, "GB/s", "hbm"
+    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": traffic_for(config, kernel),
+            "peak_kind": f"measured {peak_kind} (MEASURED_PEAKS.json)" + (" (fallback)" if pk.get("_fallback") else ""),
+            "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
+            "intensity_flop_per_byte": intensity, "ridge": ridge, "ms_per_launch": ms}
 
 
 def main():
@@ -170,15 +244,17 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="skip the per-phase profiled pass")
     ap.add_argument("--chunk-keys", type=int, default=0, help="split-K chunk cap in keys (0: library default)")
     args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
     args.gpus = max(args.gpus, world)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        wl = workload.make_workload(args.config, seed=args.seed)
+        wl = workload.make_workload(args.config, seed=args.seed, bits_only=True)
         run_reference(args, wl)
         return
 
@@ -192,13 +268,14 @@ def main():
         if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
             os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line (NCCL prints its version otherwise)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # split1 (BASELINE config 5): ONE L = 10k history split over the ranks (split-history, strong
-    # scaling, one all-gather of partials per layer); every other config: each rank its own shard
+    # split1 (BASELINE config 5): ONE L = 10k history split over the ranks (split-history, one all-gather
+    # of partials per layer); every other config: the same global request set on every rank, LPT-sharded
     split = args.config == "split1"
-    wl = workload.make_workload(args.config, seed=args.seed if split else args.seed + 1000 * rank)
-    c = wl.cfg
-    W = workload.full_weights(workload.make_workload(args.config, seed=args.seed, B=1)) if rank else \
-        workload.full_weights(wl)                                            # weights replicated (seed 0 draw)
+    gwl = workload.make_workload(args.config, seed=args.seed, bits_only=True)  # the global request set
+    c = gwl.cfg
+    mine = np.arange(len(gwl.lengths)) if split else shard_requests(gwl, world, rank)
+    wl = gwl if (split or world == 1) else workload.subset(gwl, mine, with_f32=False)  # this rank's requests
+    W = workload.full_weights(gwl)                                       # weights replicated
     model = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, dtype=c.dtype, with_z=c.with_z,
                       device=local, chunk_keys=1280 if split else args.chunk_keys,
                       split_rank=rank if split else 0, split_world=world if split else 1,
@@ -206,8 +283,8 @@ def main():
     bf16 = c.dtype == "bf16"
     Xh = wl.X_bits.view(np.int16) if bf16 else wl.X
     xth = wl.xt_bits.view(np.int16) if bf16 else wl.xt
-    X = torch.from_numpy(Xh).cuda()
-    xt = torch.from_numpy(xth).cuda()
+    X = torch.from_numpy(np.ascontiguousarray(Xh)).cuda()
+    xt = torch.from_numpy(np.ascontiguousarray(xth)).cuda()
     Z = torch.empty(wl.Nt, c.M, c.d, device="cuda")
     z = torch.empty(wl.Nt, c.d, device="cuda")
     st = torch.cuda.current_stream()
@@ -220,8 +297,6 @@ def main():
         step()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -230,33 +305,42 @@ def main():
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(st)
-        for i in range(K):
-            a, b, e = ev[i]
-            a.record(st)
-            model.project_history(X, wl.hist_off, stream=st)
-            b.record(st)
-            model.forward(xt, wl.tgt_off, Z, z, stream=st)
-            e.record(st)
+        for _ in range(K):
+            step()
         t_end.record(st)
         torch.cuda.synchronize()
     launches = (_lib.kernel_launches() - launches0) // max(K, 1)
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / K
-    proj_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
-    fwd_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
-    t = torch.tensor([ms, statistics.mean(fwd_ms)], device="cuda")
+
+    # profiled pass (separate from the timed one): per-phase CUDA events on the launching stream
+    prof = None
+    if not args.no_profile:
+        model.profile(True)
+        Kp = max(1, min(K, 5))
+        for _ in range(Kp):
+            step()
+        prof = {k: (v[0] / Kp, v[1] // Kp) for k, v in model.profile_read().items()}  # per step: (ms, regions)
+        model.profile(False)
+
+    t = torch.tensor([ms, prof["forward"][0] if prof else 0.0, prof["project"][0] if prof else 0.0,
+                      len(mine), wl.Nt, wl.T], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, fwd_max = float(t[0]), float(t[1])
-    total_targets = wl.Nt if split else wl.Nt * world
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+    else:
+        allt = [t]
+    per_rank = [[float(x) for x in a.cpu()] for a in allt]
+    ms_max = max(r[0] for r in per_rank)
+    total_targets = gwl.Nt
     value = total_targets / (ms_max * 1e-3)
 
     # e2e through the C ABI with HOST buffers (pinned), H2D/D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        Xp = torch.from_numpy(Xh).pin_memory()
-        xtp = torch.from_numpy(xth).pin_memory()
+        Xp = torch.from_numpy(np.ascontiguousarray(Xh)).pin_memory()
+        xtp = torch.from_numpy(np.ascontiguousarray(xth)).pin_memory()
         Zp = torch.empty(wl.Nt, c.M, c.d).pin_memory()
         zp = torch.empty(wl.Nt, c.d).pin_memory()
         model.project_history(Xp, wl.hist_off, stream=st)
@@ -276,38 +360,63 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": total_targets / (float(te[0]) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(Xp.numel() * Xp.element_size() + xtp.numel() * xtp.element_size()),
-               "d2h_bytes_per_step": int(Zp.numel() * 4 + zp.numel() * 4)}
+               "d2h_bytes_per_step": int(Zp.numel() * 4 + zp.numel() * 4),
+               "per": "rank 0's shard bytes; time = max over ranks" if world > 1 else "the whole step"}
 
     if rank == 0:
         pk = peaks()
-        alg = algorithmic(wl)
-        proj_avg = statistics.mean(proj_ms)
-        achieved = alg["proj_flops"] / (proj_avg * 1e-3) / 1e12
-        peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tf):
-            traffic = json.load(open(tf)).get(c.name, {}).get("projection_dram_bytes_per_launch")
+        clocks = clk.summary()
+        reasons = (clocks or {}).get("reasons", [])
+        # burst peak for a short timed region at full clocks; sustained if the power cap engaged
+        timed_s = ms * K * 1e-3
+        peak_kind = "sustained" if ("sw_power_cap" in reasons or timed_s > 1.0) else "burst"
+        alg = algorithmic(wl)  # rank 0's shard
+        kernels = []
+        if prof:
+            if prof["project"][1]:
+                kernels.append(roofline_entry("history projection (a1, k_tc_project)", "project", alg["proj_flops"],
+                                              alg["proj_bytes"], prof["project"][0] / prof["project"][1], pk,
+                                              peak_kind, c.name))
+            if prof["attention"][1]:
+                kernels.append(roofline_entry("ragged single-query attention (a4, one layer)", "attention",
+                                              alg["attn_flops_layer"], alg["attn_bytes_layer"],
+                                              prof["attention"][0] / prof["attention"][1], pk, peak_kind, c.name))
+        step_ms_prof = (prof["project"][0] + prof["forward"][0]) if prof else None
+        dom = None
+        if kernels:  # the dominant kernel by time share of the step
+            dom = max(kernels, key=lambda k: k["ms_per_launch"] * (1 if "projection" in k["kernel"] else c.M))
+        roofline = dict(dom) if dom else None
+        if roofline is not None:
+            roofline["kernels"] = kernels
+            roofline["attention"] = next((k for k in kernels if "attention" in k["kernel"]), None)
+        phases = None
+        if prof:
+            phases = {"project_ms": prof["project"][0], "forward_ms": prof["forward"][0],
+                      "attention_ms_per_layer": prof["attention"][0] / max(prof["attention"][1], 1),
+                      "merge_ms_per_layer": prof["merge"][0] / max(prof["merge"][1], 1) if prof["merge"][1] else 0.0,
+                      "target_side_ms": prof["target"][0], "target_side_launches": prof["target"][1],
+                      "targets_per_s_cached_history": wl.Nt / (prof["forward"][0] * 1e-3),
+                      "source": "stca_profile events on the launching stream (separate pass; an upper bound of "
+                                "the unprofiled step: events break programmatic-dependent-launch overlap)",
+                      "step_ms_profiled": step_ms_prof}
+        loads = [r[0] for r in per_rank]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if split else "weak",
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "bf16" if bf16 else "fp32", "data": "synthetic", "config": config_dict(wl, args),
-            "roofline": {"kernel": "history projection (a1, stca_project_history)", "bound": "tensor",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
-                         "traffic": traffic, "algorithmic_flops_per_launch": alg["proj_flops"],
-                         "ms_per_launch": proj_avg},
-            "phases": {"project_ms": proj_avg, "forward_ms": statistics.mean(fwd_ms),
-                       "forward_ms_max_over_ranks": fwd_max,
-                       "targets_per_s_cached_history": total_targets / (fwd_max * 1e-3),
-                       "attention_alg_TFLOP": alg["attn_flops"] / 1e12, "attention_alg_GB": alg["attn_bytes"] / 1e9},
+            "dtype": "bf16" if bf16 else "fp32", "data": "synthetic", "config": config_dict(gwl, args),
+            "roofline": roofline,
+            "phases": phases,
+            "ranks": {"ms_per_step": loads, "requests": [int(r[3]) for r in per_rank],
+                      "targets": [int(r[4]) for r in per_rank], "history_rows": [int(r[5]) for r in per_rank],
+                      "imbalance_max_over_mean": max(loads) / (sum(loads) / len(loads))},
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "e2e": e2e,
+            "lib_sha256": lib_sha256()[:16],
         }
         if world == 1 and not args.no_oracle:
-            line["cpu_baseline"] = oracle_sample(wl)
+            line["cpu_baseline"] = oracle_sample(gwl)
         print(json.dumps(line), flush=True)
     model.close()
     if world > 1:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define STCA_ABI_VERSION 1
+#define STCA_ABI_VERSION 2
 #define STCA_MAX_LAYERS 16
 
 typedef enum {
@@ -52,6 +52,16 @@ typedef enum {
  * recv holds split_world * bytes bytes, rank-major.  Return 0 on success. */
 typedef int (*stca_exchange_fn)(void *ctx, const void *send, void *recv, size_t bytes, void *stream);
 
+/* Device-memory provider for the handle's WORKING buffers (the projected X~ cache, staging, split-K
+ * partials, scratch; weights are allocated once at create with cudaMalloc).  alloc returns `bytes`
+ * bytes on `device` usable in stream order on `stream` (NULL on failure -> STCA_ERR_OOM); free
+ * releases a pointer from alloc once the work already enqueued on `stream` is done with it (stream
+ * order, no device synchronisation).  Buffers only grow, so a steady state of same-sized calls
+ * allocates nothing.  Both NULL: the CUDA stream-ordered pool (cudaMallocAsync / cudaFreeAsync).
+ * The Python binding passes PyTorch's caching allocator (torch.cuda.caching_allocator_alloc). */
+typedef void *(*stca_alloc_fn)(void *ctx, size_t bytes, int32_t device, void *stream);
+typedef void (*stca_free_fn)(void *ctx, void *ptr, int32_t device, void *stream);
+
 typedef struct {
   int32_t d, h, r, M;     /* model dim, heads (d % h == 0), SwiGLU ratio r >= 1, layers 1..STCA_MAX_LAYERS */
   int32_t L_infer;        /* > 0: keep the most recent L_infer rows of each history; 0: no cap */
@@ -65,6 +75,9 @@ typedef struct {
                           /* contiguous block of key chunks of every history */
   stca_exchange_fn exchange;
   void *exchange_ctx;
+  stca_alloc_fn dev_alloc; /* NULL: stream-ordered CUDA pool (see stca_alloc_fn) */
+  stca_free_fn dev_free;
+  void *alloc_ctx;
 } stca_config;
 
 /* A named weight, HOST memory, float32, row-major in the paper's row-vector
@@ -105,8 +118,12 @@ stca_status stca_create(const stca_config *cfg, const stca_tensor *weights, int3
  * work on `stream`); with L_infer truncation it is staged whole on `stream`.
  * A host X must stay valid and unmodified until `stream` has completed this
  * call's work.  hist_off is a HOST int64 array [B+1], consumed before return.
+ * The call does not wait for the device: host-side plans travel through a ring
+ * of pinned staging slots, each reused only after the event of its previous
+ * copy (so at most 8 calls may be in flight before the host waits).
  * The handle owns the projected cache until the next call or destroy.  On a
- * validation error nothing is enqueued. */
+ * validation error nothing is enqueued; on any later failure the handle has no
+ * projection (stca_forward returns STATE until the next successful call). */
 stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
                                  int64_t B, void *stream);
 
@@ -115,9 +132,10 @@ stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const
  * (request b owns target rows [tgt_off[b], tgt_off[b+1]); m_b = 0 is legal).
  * Outputs (device or host, float32): out_Z [Nt x M x d] = Z_H rows (Eq.(8)),
  * out_z [Nt x d] or NULL.  Everything is enqueued on `stream` and the call does
- * not wait: host inputs must stay valid and host outputs are complete only once
- * `stream` has completed this call's work (use pinned memory for asynchrony).
- * Any number of forwards may reuse one projection. */
+ * not wait for the device (the work list reaches it through the pinned staging
+ * ring above): host inputs must stay valid and host outputs are complete only
+ * once `stream` has completed this call's work (use pinned memory for
+ * asynchrony).  Any number of forwards may reuse one projection. */
 stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                          float *out_Z, float *out_z, void *stream);
 
@@ -127,6 +145,20 @@ stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64
  * (device or host; a host copy completes before return).  STATE before any projection,
  * INVALID_ARG for a layer or row range outside the cache. */
 stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t row0, int64_t nrows, float *out, void *stream);
+
+/* ---- per-phase device timing (bench.py's roofline evidence) ----
+ * enable != 0: every later project / forward call records CUDA events on its stream around each
+ * phase: STCA_PH_PROJECT (a1, the history projection), STCA_PH_ATTENTION (a4: the attention
+ * launches of one layer = one region), STCA_PH_MERGE (the split-K fold of one layer),
+ * STCA_PH_TARGET (a2/a3/a5-a7: the target-side GEMM launches, one region per launch) and
+ * STCA_PH_FORWARD (a whole stca_forward).  Events between kernels remove the programmatic-
+ * dependent-launch overlap across them, so profiled phase times are upper bounds of unprofiled
+ * ones.  stca_profile_read waits for the recorded events, writes the total milliseconds and the
+ * region count of every phase since the last read (arrays of STCA_PH_N) and resets. */
+enum { STCA_PH_PROJECT = 0, STCA_PH_ATTENTION = 1, STCA_PH_MERGE = 2, STCA_PH_TARGET = 3, STCA_PH_FORWARD = 4,
+       STCA_PH_N = 5 };
+stca_status stca_profile(stca_handle *h, int32_t enable);
+stca_status stca_profile_read(stca_handle *h, double *ms, int64_t *count);
 
 void stca_destroy(stca_handle *h);                  /* NULL-safe; synchronises the device */
 const char *stca_last_error(const stca_handle *h);  /* last non-OK message; h == NULL: last failed create on this thread */
@@ -176,8 +208,8 @@ void stca_plan_persistent(const int64_t *cost, int64_t n, int32_t n_ctas, int32_
 
 /* Per request b < B: L_train_b = 8 * floor((L_min + s_b (L_max - L_min)) / 8 + 1/2) (Eq. beta-scale
  * P:L258 + P:L260, fp64; s_b ~ Beta(alpha, beta) drawn by the caller, in [0, 1]); the temporal suffix
- * request req_b = min(L_train_b, n_b), n_b = hist_off[b+1] - hist_off[b] (P:L275); the global length
- * allocation alloc[b] <= req_b with sum(alloc) <= B * L_avg (P:L281-283); new_off [B+1] = exclusive
+ * request req_b = min(L_train_b, n_b), n_b = hist_off[b+1] - hist_off[b] (P:L279); the global length
+ * allocation alloc[b] <= req_b with sum(alloc) <= B * L_avg (P:L286); new_off [B+1] = exclusive
  * prefix sum of alloc, the ragged index over the compacted rows.
  * Synchronises `stream` (reads a device status word).  INVALID_ARG for B outside [1, 49152],
  * L_min > L_max, L_avg < 1, an s_b outside [0, 1] or an infeasible budget (sum of min(req_b, 8) >
@@ -185,7 +217,7 @@ void stca_plan_persistent(const int64_t *cost, int64_t n, int32_t n_ctas, int32_
 stca_status stca_rlb_allocate(const double *s, const int64_t *hist_off, int64_t B, int32_t L_min, int32_t L_max,
                               int32_t L_avg, int64_t *alloc, int64_t *new_off, void *stream);
 
-/* Sequence compaction (P:L284): the last alloc[b] rows of request b's history in X [T x row_bytes]
+/* Sequence compaction (P:L287): the last alloc[b] rows of request b's history in X [T x row_bytes]
  * (rows hist_off[b+1] - alloc[b] .. hist_off[b+1] - 1) are copied, back to back in request order, to
  * P [new_off[B] x row_bytes], viewed as physical rows of L_avg tokens laid end to end.  The segment
  * map: segs [n_seg x 3] int64 (row, start, len) triples, those of request b at seg_off[b] ..

@@ -9,12 +9,12 @@ Steps, in the paper's order (§3.3 "Subsequence selection" and "Batch-L
 1. train_lengths  -- Eq.(beta-scale) P:L255-258 and the rounding sentence P:L260: L_raw = L_min +
    s (L_max - L_min), rounded to the nearest multiple of 8.  s ~ Beta(alpha, beta) is drawn by the
    caller and passed in (reading R-N2a); beta_shape() is Eq.(beta) P:L266-269.
-2. requested      -- the temporal suffix (P:L275): request b keeps min(L_train_b, n_b) of its n_b rows.
-3. allocate       -- "Global Length Allocation" P:L281-283 against the budget B * L_avg.  The paper gives
+2. requested      -- the temporal suffix (P:L279): request b keeps min(L_train_b, n_b) of its n_b rows.
+3. allocate       -- "Global Length Allocation" P:L286 against the budget B * L_avg.  The paper gives
    no algorithm; the reading (DESIGN.md R-N2b, after SPEC's allocation design decision) is exact
    integer proportional scaling floored to multiples of 8, a floor of min(req_b, 8), then one +8 per
    sequence to the most-truncated sequences (ties: lowest index) while the slack allows.
-4. compact        -- "Sequence Compaction" P:L284: the kept suffixes packed back to back into physical
+4. compact        -- "Sequence Compaction" P:L287: the kept suffixes packed back to back into physical
    rows of exactly L_avg tokens, a sequence split across adjacent rows where needed (greedy first-fit
    in input order, SPEC's packing rule); the segment map holds (row, start, len) triples per sequence
    and the ragged index is the exclusive prefix sum of the allocated lengths.
@@ -42,7 +42,7 @@ def train_lengths(s, L_min: int, L_max: int) -> np.ndarray:
 
 
 def requested(L_train, hist_off) -> np.ndarray:
-    """P:L275: keep the most recent min(L_train_b, n_b) rows of request b (n_b = its history length)."""
+    """P:L279: keep the most recent min(L_train_b, n_b) rows of request b (n_b = its history length)."""
     B = len(L_train)
     return np.array([min(int(L_train[b]), int(hist_off[b + 1]) - int(hist_off[b])) for b in range(B)],
                     dtype=np.int64)
@@ -53,7 +53,7 @@ class InfeasibleBudget(ValueError):
 
 
 def allocate(req, budget: int) -> np.ndarray:
-    """Global length allocation P:L281-283, reading R-N2b.  Exact integers throughout."""
+    """Global length allocation P:L286, reading R-N2b.  Exact integers throughout."""
     req = [int(v) for v in req]
     B = len(req)
     total = sum(req)
@@ -78,7 +78,7 @@ def allocate(req, budget: int) -> np.ndarray:
 
 
 def compact(X, hist_off, alloc, L_avg: int):
-    """Sequence compaction P:L284 (+ ragged index P:L289).
+    """Sequence compaction P:L287 (+ ragged index P:L289).
 
     X [T x d] (any dtype; rows are copied, never changed), hist_off [B+1], alloc [B].
     Returns (P, new_off, seg_off, segs): P [sum(alloc) x d] -- the physical rows of L_avg tokens laid

@@ -19,8 +19,8 @@ from typing import Dict, Optional
 import numpy as np
 
 from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_persistent, plan_shards,  # noqa: F401,E501
-                   plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, _Config,
-                   _Tensor, LIB_PATH)
+                   plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, ALLOC_FN,
+                   FREE_FN, PHASES, _Config, _Tensor, LIB_PATH)
 
 __all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_persistent", "plan_shards", "plan_split", "plan_suffix",
            "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange", "rlb_allocate",
@@ -73,12 +73,33 @@ def _i64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
 
 
+def _torch_allocator():
+    """stca_alloc_fn / stca_free_fn over PyTorch's CUDA caching allocator (stream-ordered blocks)."""
+    import torch
+
+    def alloc(ctx, nbytes, device, stream):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=int(device), stream=int(stream or 0))
+        except Exception:  # OOM -> NULL -> STCA_ERR_OOM
+            return None
+
+    def free(ctx, ptr, device, stream):
+        try:
+            torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:  # pragma: no cover  (interpreter shutdown)
+            pass
+    return ALLOC_FN(alloc), FREE_FN(free)
+
+
 class STCA:
     """One handle = one device's copy of the weights + the projected history cache."""
 
     def __init__(self, weights: Dict[str, np.ndarray], *, d: int, h: int, r: int, M: int, L_infer: int = 0,
                  dtype: str = "bf16", with_z: bool = True, device: int = 0, chunk_keys: int = 0,
-                 ln_eps: float = 1e-5, split_rank: int = 0, split_world: int = 1, exchange=None):
+                 ln_eps: float = 1e-5, split_rank: int = 0, split_world: int = 1, exchange=None,
+                 allocator: str = "torch"):
+        """allocator: "torch" (working buffers from PyTorch's caching allocator) or "cuda" (the
+        library's stream-ordered CUDA pool)."""
         self.d, self.h, self.r, self.M, self.with_z = d, h, r, M, with_z
         self.dtype = dtype
         cfg = _Config()
@@ -94,6 +115,12 @@ class STCA:
         if exchange is not None:
             self._exchange_cb = EXCHANGE_FN(exchange)
             cfg.exchange = self._exchange_cb
+        self._alloc_cbs = None
+        if allocator == "torch":
+            self._alloc_cbs = _torch_allocator()
+            cfg.dev_alloc, cfg.dev_free = self._alloc_cbs
+        elif allocator != "cuda":
+            raise ValueError(f"allocator must be 'torch' or 'cuda', not {allocator!r}")
         # weights: host float32; identical array objects keep identical pointers (reading R5 aliasing)
         conv, keep = {}, []
         tens = (_Tensor * len(weights))()
@@ -131,6 +158,22 @@ class STCA:
     def _check(self, rc):
         if rc != 0:
             raise StcaError(rc, lib().stca_last_error(self._h).decode())
+
+    def debug_capture(self, layer: int, U, Y) -> None:
+        """Test hook: the next forward copies layer `layer`'s U and Y (storage dtype, [Nt h x d]) into the
+        given CUDA tensors."""
+        self._check(lib().stca_debug_capture(self._h, int(layer), ctypes.c_void_p(_ptr(U)), ctypes.c_void_p(_ptr(Y))))
+
+    # -- per-phase device timing (stca_profile) --
+    def profile(self, enable: bool = True) -> None:
+        self._check(lib().stca_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{phase: (total ms, regions)} since the last read (waits for the recorded events)."""
+        ms = (ctypes.c_double * len(PHASES))()
+        n = np.zeros(len(PHASES), dtype=np.int64)
+        self._check(lib().stca_profile_read(self._h, ms, n.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(PHASES)}
 
     # -- the two calls --
     def project_history(self, X, hist_off, stream=None) -> None:
@@ -257,7 +300,7 @@ def rlb_allocate(s, hist_off, L_min: int, L_max: int, L_avg: int, stream=None):
 
 
 def rlb_compact(X, hist_off, alloc, new_off, L_avg: int, P=None, stream=None):
-    """stca_rlb_compact (include/stca.h; P:L284-289): X CUDA tensor [T x d] (any 2-D dtype, rows of a
+    """stca_rlb_compact (include/stca.h; P:L287-289): X CUDA tensor [T x d] (any 2-D dtype, rows of a
     multiple of 16 bytes).  Returns (P [B*L_avg x d] with rows < new_off[B] written, seg_off [B+1],
     segs [2B x 3]) as CUDA tensors; the number of valid triples is seg_off[B]."""
     import torch

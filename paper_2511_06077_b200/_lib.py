@@ -12,6 +12,10 @@ STCA_BF16, STCA_FP32 = 0, 1
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                ctypes.c_void_p)
+# stca_alloc_fn / stca_free_fn (working-buffer provider)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p)
+PHASES = ["project", "attention", "merge", "target", "forward"]  # STCA_PH_* order
 
 
 class _Config(ctypes.Structure):
@@ -19,7 +23,8 @@ class _Config(ctypes.Structure):
                 ("L_infer", ctypes.c_int32), ("ln_eps", ctypes.c_float), ("dtype", ctypes.c_int32),
                 ("with_z", ctypes.c_int32), ("device", ctypes.c_int32), ("chunk_keys", ctypes.c_int32),
                 ("split_rank", ctypes.c_int32), ("split_world", ctypes.c_int32), ("exchange", EXCHANGE_FN),
-                ("exchange_ctx", ctypes.c_void_p)]
+                ("exchange_ctx", ctypes.c_void_p), ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN),
+                ("alloc_ctx", ctypes.c_void_p)]
 
 
 class _Tensor(ctypes.Structure):
@@ -39,7 +44,8 @@ _I64P = ctypes.POINTER(ctypes.c_int64)
 SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy", "stca_last_error",
            "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
-           "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact"]
+           "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact",
+           "stca_profile", "stca_profile_read"]
 
 
 def lib():
@@ -94,6 +100,14 @@ def lib():
         L.stca_read_cache.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                       ctypes.c_void_p]
         L.stca_read_cache.restype = ctypes.c_int
+        L.stca_debug_capture.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        L.stca_debug_capture.restype = ctypes.c_int32
+        L.stca_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.stca_profile.restype = ctypes.c_int32
+        L.stca_profile_read.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _I64P]
+        L.stca_profile_read.restype = ctypes.c_int32
+        if L.stca_abi_version() != 2:
+            raise ImportError(f"{LIB_PATH}: ABI version {L.stca_abi_version()}, this binding speaks 2 (rebuild)")
         _lib = L
     return _lib
 

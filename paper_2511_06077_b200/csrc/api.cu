@@ -30,21 +30,50 @@ void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 
+// Working-buffer provider of a handle (stca_alloc_fn, include/stca.h): the caller's (e.g. PyTorch's
+// caching allocator) or the CUDA stream-ordered pool.  Never synchronises the device.
+struct Alloc {
+  stca_alloc_fn fa = nullptr;
+  stca_free_fn ff = nullptr;
+  void *ctx = nullptr;
+  int dev = 0;
+  cudaError_t get(void **p, size_t bytes, cudaStream_t st) const {
+    if (fa) {
+      *p = fa(ctx, bytes, dev, (void *)st);
+      return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
+    return cudaMallocAsync(p, bytes, st);
+  }
+  void put(void *p, cudaStream_t st) const {
+    if (!p) return;
+    if (ff)
+      ff(ctx, p, dev, (void *)st);
+    else
+      cudaFreeAsync(p, st);
+  }
+};
+
+// A grow-only device buffer; the old block is released in stream order on the stream that grows it
+// (work already enqueued there may still read it).
 struct DevBuf {
   void *p = nullptr;
   size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
+  const Alloc *al = nullptr;
+  cudaError_t ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
+    al->put(p, st);
     p = nullptr;
     cap = 0;
     size_t want = bytes + bytes / 8 + 256;
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) cap = want;
+    cudaError_t e = al->get(&p, want, st);
+    if (e == cudaSuccess)
+      cap = want;
+    else
+      p = nullptr;
     return e;
   }
-  void release() {
-    if (p) cudaFree(p);
+  void release() {  // the device is idle (stca_destroy)
+    if (p && al) al->put(p, 0);
     p = nullptr;
     cap = 0;
   }
@@ -69,6 +98,29 @@ struct HostPinned {
     p = nullptr;
     cap = 0;
   }
+};
+
+// Pinned staging ring for host-side plans (work lists, gather segments): slot k is reused (and
+// possibly regrown) only after the event recorded behind its last H2D copy, so a call never waits
+// for the device unless STAGING_SLOTS calls are still in flight.
+constexpr int STAGING_SLOTS = 8;
+struct StagingRing {
+  HostPinned buf[STAGING_SLOTS];
+  cudaEvent_t ev[STAGING_SLOTS] = {};
+  int next = 0;
+  void release() {
+    for (int k = 0; k < STAGING_SLOTS; ++k) {
+      buf[k].release();
+      if (ev[k]) cudaEventDestroy(ev[k]);
+      ev[k] = nullptr;
+    }
+  }
+};
+
+// Per-phase event regions (stca_profile)
+struct ProfRegion {
+  int phase;
+  cudaEvent_t a, b;
 };
 
 }  // namespace
@@ -100,16 +152,63 @@ struct stca_handle {
   std::vector<int64_t> start, len, coff;  // start'_b (input rows), L'_b, compacted offsets [B+1]
   std::vector<int64_t> own0, olen;         // split-history: first owned key and owned key count (else 0, L'_b)
   int64_t T2 = 0;
+  Alloc al;
   DevBuf xt_cache;  // M x [T2 x d] storage
   DevBuf xin, xgather, seg, proj_h, proj_y;
   // forward scratch
   DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, ctal, zout, Zout;
-  HostPinned pin;
+  StagingRing stage;
+  // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
+  int cap_layer = 0;
+  void *cap_U = nullptr, *cap_Y = nullptr;
+  // stca_profile
+  bool prof = false;
+  std::vector<ProfRegion> prof_open;  // recorded, not yet read
+  std::vector<cudaEvent_t> prof_pool;
   int64_t chunk_cap = STCA_DEFAULT_CHUNK_KEYS;
   // pipelined host-input projection: copy stream + one event per piece
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_xin_free = nullptr, ev[STCA_H2D_PIECES] = {};
 };
+
+static DevBuf *const *all_bufs(stca_handle *h, int *n) {
+  static thread_local DevBuf *v[32];
+  DevBuf *list[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
+                    &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
+                    &h->part,     &h->partg, &h->items,  &h->mitems, &h->ctal,   &h->zout,   &h->Zout};
+  *n = (int)(sizeof list / sizeof list[0]);
+  for (int i = 0; i < *n; ++i) v[i] = list[i];
+  return v;
+}
+
+// ---- stca_profile: event regions on the launching stream ----
+static cudaEvent_t prof_begin(stca_handle *h, cudaStream_t st) {
+  if (!h->prof) return nullptr;
+  cudaEvent_t e = nullptr;
+  if (!h->prof_pool.empty()) {
+    e = h->prof_pool.back();
+    h->prof_pool.pop_back();
+  } else if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaEventRecord(e, st);
+  return e;
+}
+static void prof_end(stca_handle *h, int phase, cudaEvent_t a, cudaStream_t st) {
+  if (!a) return;
+  cudaEvent_t b = nullptr;
+  if (!h->prof_pool.empty()) {
+    b = h->prof_pool.back();
+    h->prof_pool.pop_back();
+  } else if (cudaEventCreate(&b) != cudaSuccess) {
+    cudaGetLastError();
+    h->prof_pool.push_back(a);
+    return;
+  }
+  cudaEventRecord(b, st);
+  h->prof_open.push_back({phase, a, b});
+}
 
 static thread_local std::string g_create_error;  // message of the last failed stca_create on this thread
 
@@ -371,10 +470,25 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
   h->bf16 = cfg->dtype == STCA_BF16;
   h->es = h->bf16 ? 2 : 4;
   h->chunk_cap = cfg->chunk_keys > 0 ? cfg->chunk_keys : STCA_DEFAULT_CHUNK_KEYS;
+  if ((cfg->dev_alloc == nullptr) != (cfg->dev_free == nullptr))
+    return bad(fail(h, STCA_ERR_INVALID_ARG, "dev_alloc and dev_free must both be set or both be NULL"));
+  h->al.fa = cfg->dev_alloc;
+  h->al.ff = cfg->dev_free;
+  h->al.ctx = cfg->alloc_ctx;
+  h->al.dev = cfg->device;
+  {
+    int n = 0;
+    DevBuf *const *v = all_bufs(h, &n);
+    for (int i = 0; i < n; ++i) v[i]->al = &h->al;
+  }
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     cudaGetLastError();
     return bad(fail(h, STCA_ERR_CUDA, "cudaSetDevice(%d) failed", cfg->device));
   }
+  // the bf16 path is tcgen05-only: no CUDA-core substitute for its GEMMs / projection
+  if (h->bf16 && !stca::tc_available())
+    return bad(fail(h, STCA_ERR_UNSUPPORTED, "the bf16 path needs an sm_100a (B200) device; device %d is not one",
+                    cfg->device));
 
   // ---- collect and validate names / shapes ----
   std::map<std::string, const stca_tensor *> byname;
@@ -542,11 +656,16 @@ extern "C" void stca_destroy(stca_handle *h) {
   cudaSetDevice(h->cfg.device);
   cudaDeviceSynchronize();
   for (void *p : h->allocs) cudaFree(p);
-  DevBuf *bufs[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,   &h->proj_h, &h->proj_y, &h->xtin,
-                    &h->ocat,     &h->q,    &h->c,       &h->hbuf,  &h->ybuf32, &h->U,      &h->Y,
-                    &h->part,     &h->partg, &h->items, &h->mitems, &h->ctal, &h->zout,  &h->Zout};
-  for (DevBuf *b : bufs) b->release();
-  h->pin.release();
+  int nb = 0;
+  DevBuf *const *bufs = all_bufs(h, &nb);
+  for (int i = 0; i < nb; ++i) bufs[i]->release();
+  cudaDeviceSynchronize();  // stream-ordered frees on the legacy stream
+  h->stage.release();
+  for (ProfRegion &r : h->prof_open) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : h->prof_pool) cudaEventDestroy(e);
   if (h->copy_st) {
     cudaStreamDestroy(h->copy_st);
     cudaEventDestroy(h->ev_xin_free);
@@ -558,6 +677,20 @@ extern "C" void stca_destroy(stca_handle *h) {
 
 extern "C" const char *stca_last_error(const stca_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
+// A pinned staging slot of at least `bytes` bytes for host -> device copies enqueued on `st`; the
+// caller records *ev on `st` after its copies.  Waits only if the slot's previous copy is unfinished.
+static stca_status staging_acquire(stca_handle *h, size_t bytes, void **out, cudaEvent_t *ev) {
+  StagingRing &r = h->stage;
+  const int k = r.next;
+  r.next = (k + 1) % STAGING_SLOTS;
+  if (!r.ev[k]) CU(cudaEventCreateWithFlags(&r.ev[k], cudaEventDisableTiming));
+  CU(cudaEventSynchronize(r.ev[k]));  // the slot's last copy has read it (normally long done)
+  CU(r.buf[k].ensure(bytes));
+  *out = r.buf[k].p;
+  *ev = r.ev[k];
+  return STCA_OK;
+}
+
 // ===========================================================================
 // project_history
 // ===========================================================================
@@ -567,7 +700,7 @@ static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64
   const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
   const size_t row_bytes = (size_t)d * es;
   const int64_t T2 = h->T2;
-  if (h->bf16 && stca::tc_available()) {
+  if (h->bf16) {  // tcgen05 (stca_create refused bf16 without an sm_100a device)
     stca::TcProj pj;
     pj.X = X;
     pj.rows = rows;
@@ -587,12 +720,19 @@ static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64
       pj.g[i] = h->L[i].gh;
       pj.b[i] = h->L[i].bh;
     }
+    if (d != 128) {  // two-GEMM path: the handle's H scratch, pieces of at most 2^18 rows
+      pj.H_rows = std::min<int64_t>(rows, 1 << 18);
+      CU(h->proj_h.ensure((size_t)pj.H_rows * rd * 2, st));
+      pj.H = h->proj_h.p;
+    }
+    cudaEvent_t pa = prof_begin(h, st);
     CU(stca::tc_project(pj, st));
+    prof_end(h, STCA_PH_PROJECT, pa, st);
     return STCA_OK;
   }
   const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
-  CU(h->proj_h.ensure((size_t)R * rd * es));
-  CU(h->proj_y.ensure((size_t)R * d * 4));
+  CU(h->proj_h.ensure((size_t)R * rd * es, st));
+  CU(h->proj_y.ensure((size_t)R * d * 4, st));
   for (int i = 0; i < M; ++i) {
     for (int64_t q0 = 0; q0 < rows; q0 += R) {
       const int n = (int)std::min<int64_t>(R, rows - q0);
@@ -629,8 +769,9 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
   }
   CU(cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
-  const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
+  const int d = h->cfg.d, M = h->cfg.M, es = h->es;
   const size_t row_bytes = (size_t)d * es;
+  h->B = -1;  // no valid projection until this call has enqueued all of its work (a failure below leaves none)
 
   // a0: suffix truncation + compacted offsets (exact integer work)
   h->start.assign(B, 0);
@@ -650,19 +791,22 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     gather |= h->start[b] + h->own0[b] != hist_off[b] || h->olen[b] != hist_off[b + 1] - hist_off[b];
   }
   const int64_t T2 = h->coff[B];  // rows of the X~ cache (the suffix rows this rank owns)
-  CU(h->xt_cache.ensure((size_t)M * T2 * row_bytes + 256));
+  CU(h->xt_cache.ensure((size_t)M * T2 * row_bytes + 256, st));
   h->T2 = T2;
   const void *Xd = X;
   const bool host_x = T > 0 && !is_device_ptr(X);
   if (host_x && !gather && T2 > 0) {
     // host input, no gather: stream X up in pieces on a copy stream and project each piece as soon as
     // it has landed, so the H2D copy (the e2e bottleneck) overlaps the projection of earlier pieces
-    CU(h->xin.ensure((size_t)T * row_bytes));
     if (!h->copy_st) {
       CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&h->ev_xin_free, cudaEventDisableTiming));
       for (cudaEvent_t &e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    void *const xin_old = h->xin.p;
+    CU(h->xin.ensure((size_t)T * row_bytes, st));
+    // a regrown xin was allocated in `stream` order: the copy stream may write it only after that point
+    if (h->xin.p != xin_old) CU(cudaEventRecord(h->ev_xin_free, st));
     // the copies only wait for the previous projection's reads of xin (ev_xin_free), not for other
     // work on `stream`: the next request batch's upload overlaps the current forward
     CU(cudaStreamWaitEvent(h->copy_st, h->ev_xin_free, 0));
@@ -684,7 +828,7 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     return STCA_OK;
   }
   if (host_x) {  // host input with a gather: stage all of X on the stream first
-    CU(h->xin.ensure((size_t)T * row_bytes));
+    CU(h->xin.ensure((size_t)T * row_bytes, st));
     CU(cudaMemcpyAsync(h->xin.p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
     Xd = h->xin.p;
   }
@@ -697,12 +841,15 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
       seg.push_back(h->olen[b]);
       maxlen = std::max(maxlen, h->olen[b]);
     }
-    CU(h->seg.ensure(seg.size() * 8));
-    CU(h->pin.ensure(seg.size() * 8));
-    CU(cudaStreamSynchronize(st));  // pinned staging reuse
-    memcpy(h->pin.p, seg.data(), seg.size() * 8);
-    CU(cudaMemcpyAsync(h->seg.p, h->pin.p, seg.size() * 8, cudaMemcpyHostToDevice, st));
-    CU(h->xgather.ensure((size_t)T2 * row_bytes));
+    CU(h->seg.ensure(seg.size() * 8, st));
+    void *slot = nullptr;
+    cudaEvent_t slot_ev = nullptr;
+    stca_status ss = staging_acquire(h, seg.size() * 8, &slot, &slot_ev);
+    if (ss != STCA_OK) return ss;
+    memcpy(slot, seg.data(), seg.size() * 8);
+    CU(cudaMemcpyAsync(h->seg.p, slot, seg.size() * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(slot_ev, st));
+    CU(h->xgather.ensure((size_t)T2 * row_bytes, st));
     CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), B, maxlen, (int)row_bytes, st));
     Xd = h->xgather.p;
   }
@@ -724,13 +871,16 @@ static stca_status ffn_rows(stca_handle *h, const void *in, int64_t ldi, int64_t
   // SwiGLUFFN (+ LN when g != null) on `rows` rows: the query-side instances of Eq.(1), (3), (7), (9)
   const int d = h->cfg.d, rd = h->cfg.r * d, es = h->es;
   if (rows <= 0) return STCA_OK;
-  if (h->bf16 && stca::tc_available()) {
+  if (h->bf16) {
+    CU(h->hbuf.ensure((size_t)rows * rd * 2, st));  // H scratch owned by this handle
+    cudaEvent_t pa = prof_begin(h, st);
     CU(stca::tc_ffn(in, ldi, rows, which == 0 ? tcw->W1h : tcw->W1q, which == 0 ? tcw->Woh : tcw->Woq, d, rd, g, b,
-                    h->cfg.ln_eps, out_s, ldo, out_f, ldof, st));
+                    h->cfg.ln_eps, out_s, ldo, out_f, ldof, h->hbuf.p, st));
+    prof_end(h, STCA_PH_TARGET, pa, st);
     return STCA_OK;
   }
-  CU(h->hbuf.ensure((size_t)rows * rd * es));
-  CU(h->ybuf32.ensure((size_t)rows * d * 4));
+  CU(h->hbuf.ensure((size_t)rows * rd * es, st));
+  CU(h->ybuf32.ensure((size_t)rows * d * 4, st));
   CU(stca::cc_gemm(h->bf16, in, ldi, W1, 2 * rd, h->hbuf.p, rd, nullptr, 0, (int)rows, 2 * rd, d, 1.f,
                    stca::EPI_SWIGLU, st));
   if (g) {
@@ -747,8 +897,10 @@ static stca_status ffn_rows(stca_handle *h, const void *in, int64_t ldi, int64_t
 static stca_status gemm(stca_handle *h, const void *A, int64_t lda, const void *Bw, const void *Btc, int64_t ldb,
                         void *Cs, int64_t ldcs, float *Cf, int64_t ldcf, int64_t M, int N, int K, cudaStream_t st) {
   if (M <= 0) return STCA_OK;
-  if (h->bf16 && stca::tc_available()) {
+  if (h->bf16) {
+    cudaEvent_t pa = prof_begin(h, st);
     CU(stca::tc_gemm(A, lda, Btc, M, N, K, Cs, ldcs, Cf, ldcf, st));
+    prof_end(h, STCA_PH_TARGET, pa, st);
     return STCA_OK;
   }
   CU(stca::cc_gemm(h->bf16, A, lda, Bw, ldb, Cs, ldcs, Cf, ldcf, (int)M, N, K, 1.f, stca::EPI_STORE, st));
@@ -777,7 +929,7 @@ extern "C" stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t ro
   const bool host = !is_device_ptr(out);
   float *dst = out;
   if (host) {
-    CU(h->Zout.ensure(n * 4));
+    CU(h->Zout.ensure(n * 4, st));
     dst = h->Zout.as<float>();
   }
   if (h->bf16)
@@ -790,6 +942,9 @@ extern "C" stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t ro
   }
   return STCA_OK;
 }
+
+static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                                float *out_Z, float *out_z, cudaStream_t st);
 
 extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                                     float *out_Z, float *out_z, void *stream) {
@@ -807,6 +962,15 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   if (Nt == 0) return STCA_OK;
   CU(cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t p_fwd = prof_begin(h, st);
+  s = forward_body(h, xt, Nt, tgt_off, B, out_Z, out_z, st);
+  if (s == STCA_OK) prof_end(h, STCA_PH_FORWARD, p_fwd, st);
+  return s;
+}
+
+static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                                float *out_Z, float *out_z, cudaStream_t st) {
+  stca_status s = STCA_OK;
   const int d = h->cfg.d, hh = h->cfg.h, M = h->cfg.M, es = h->es;
   const int64_t NQ = Nt * hh;  // query rows (target, head)
   const int64_t ldo = (int64_t)(M + 1) * d;
@@ -814,30 +978,30 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   // inputs: x_t into block 0 of the concatenation buffer [x_t | o1 | ... | oM] (R10)
   const void *xtd = xt;
   if (!is_device_ptr(xt)) {
-    CU(h->xtin.ensure((size_t)Nt * d * es));
+    CU(h->xtin.ensure((size_t)Nt * d * es, st));
     CU(cudaMemcpyAsync(h->xtin.p, xt, (size_t)Nt * d * es, cudaMemcpyHostToDevice, st));
     xtd = h->xtin.p;
   }
   float *Zd = out_Z, *zd = out_z;
   const bool Z_host = !is_device_ptr(out_Z), z_host = out_z && !is_device_ptr(out_z);
   if (Z_host) {
-    CU(h->Zout.ensure((size_t)Nt * M * d * 4));
+    CU(h->Zout.ensure((size_t)Nt * M * d * 4, st));
     Zd = h->Zout.as<float>();
   }
   if (z_host) {
-    CU(h->zout.ensure((size_t)Nt * d * 4));
+    CU(h->zout.ensure((size_t)Nt * d * 4, st));
     zd = h->zout.as<float>();
   }
-  CU(h->ocat.ensure((size_t)Nt * ldo * es));
-  CU(h->q.ensure((size_t)Nt * d * es));
-  CU(h->c.ensure((size_t)Nt * d * es));
-  CU(h->U.ensure((size_t)NQ * d * es));
-  CU(h->Y.ensure((size_t)NQ * d * es));
+  CU(h->ocat.ensure((size_t)Nt * ldo * es, st));
+  CU(h->q.ensure((size_t)Nt * d * es, st));
+  CU(h->c.ensure((size_t)Nt * d * es, st));
+  CU(h->U.ensure((size_t)NQ * d * es, st));
+  CU(h->Y.ensure((size_t)NQ * d * es, st));
   CU(stca::copy_rows_strided(xtd, (int64_t)d * es, h->ocat.p, ldo * es, Nt, d * es, st));
 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
-  const bool tc_attn = h->bf16 && stca::tc_available() && stca::tc_attention_supported(d);
-  const bool tc_wide = h->bf16 && stca::tc_available() && stca::tc_attention_wide_supported(d);
+  const bool tc_attn = h->bf16 && stca::tc_attention_supported(d);
+  const bool tc_wide = h->bf16 && stca::tc_attention_wide_supported(d);
   // A request with at most 64 query rows (m_b h) takes the transposed kernel (keys = MMA rows), which
   // does not pad it to a 128-row query tile.  The choice is PER REQUEST (its items are moved behind
   // the others and launched separately), so a request's arithmetic never depends on its batch
@@ -913,21 +1077,27 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   }
   const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
   const size_t ctal_bytes = ctal.size() * sizeof(int32_t);
-  CU(h->items.ensure(items_bytes + 64));
-  CU(h->mitems.ensure(mi_bytes + 64));
-  CU(h->ctal.ensure(ctal_bytes + 64));
-  CU(h->pin.ensure(items_bytes + mi_bytes + ctal_bytes + 64));
-  CU(cudaStreamSynchronize(st));  // the pinned staging buffer may still feed an earlier copy
-  memcpy(h->pin.p, items.data(), items_bytes);
-  memcpy((uint8_t *)h->pin.p + items_bytes, mi.data(), mi_bytes);
-  memcpy((uint8_t *)h->pin.p + items_bytes + mi_bytes, ctal.data(), ctal_bytes);
-  if (items_bytes) CU(cudaMemcpyAsync(h->items.p, h->pin.p, items_bytes, cudaMemcpyHostToDevice, st));
-  if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, (uint8_t *)h->pin.p + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
-  if (ctal_bytes)
-    CU(cudaMemcpyAsync(h->ctal.p, (uint8_t *)h->pin.p + items_bytes + mi_bytes, ctal_bytes, cudaMemcpyHostToDevice, st));
+  CU(h->items.ensure(items_bytes + 64, st));
+  CU(h->mitems.ensure(mi_bytes + 64, st));
+  CU(h->ctal.ensure(ctal_bytes + 64, st));
+  {  // the plan reaches the device through a pinned staging slot: no host wait
+    void *slot = nullptr;
+    cudaEvent_t slot_ev = nullptr;
+    s = staging_acquire(h, items_bytes + mi_bytes + ctal_bytes + 64, &slot, &slot_ev);
+    if (s != STCA_OK) return s;
+    uint8_t *pin = (uint8_t *)slot;
+    memcpy(pin, items.data(), items_bytes);
+    memcpy(pin + items_bytes, mi.data(), mi_bytes);
+    memcpy(pin + items_bytes + mi_bytes, ctal.data(), ctal_bytes);
+    if (items_bytes) CU(cudaMemcpyAsync(h->items.p, pin, items_bytes, cudaMemcpyHostToDevice, st));
+    if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, pin + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
+    if (ctal_bytes)
+      CU(cudaMemcpyAsync(h->ctal.p, pin + items_bytes + mi_bytes, ctal_bytes, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(slot_ev, st));
+  }
   const size_t part_bytes = (size_t)part_rows * stca::part_row_bytes(d, es);
-  if (part_rows) CU(h->part.ensure(part_bytes));
-  if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G));
+  if (part_rows) CU(h->part.ensure(part_bytes, st));
+  if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G, st));
 
   // a2: q(1) = LN(SwiGLUFFN(1)(x_t)), Eq.(3)
   LayerW &L1 = h->L[0];
@@ -940,6 +1110,7 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
+    cudaEvent_t pa = prof_begin(h, st);
     if (tc_attn) {
       if (nit_nar > 0)
         CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg,
@@ -954,14 +1125,25 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     }
+    prof_end(h, STCA_PH_ATTENTION, pa, st);
     const float *merged_from = h->part.as<float>();
     if (G > 1 && part_rows) {  // split-history exchange: all-gather every rank's partials (one step per layer)
       if (h->cfg.exchange(h->cfg.exchange_ctx, h->part.p, h->partg.p, part_bytes, (void *)st) != 0)
         return fail(h, STCA_ERR_COMM, "split-history exchange failed at layer %d", i);
       merged_from = h->partg.as<float>();
     }
+    if (h->cap_layer == i) {  // stage-isolated test hook: this layer's U (a3 output) and Y (a4 output)
+      CU(cudaMemcpyAsync(h->cap_U, h->U.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
+    }
+    pa = prof_begin(h, st);
     CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
                             G, (int64_t)part_bytes, h->Y.p, st));
+    if (!mi.empty()) prof_end(h, STCA_PH_MERGE, pa, st);
+    else if (pa) h->prof_pool.push_back(pa);
+    if (h->cap_layer == i) {
+      CU(cudaMemcpyAsync(h->cap_Y, h->Y.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
+      h->cap_layer = 0;
+    }
     // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
     s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,
              Zd + (size_t)(i - 1) * d, (int64_t)M * d, Nt, d, hh * d, st);
@@ -986,5 +1168,46 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   if (z_host) CU(cudaMemcpyAsync(out_z, zd, (size_t)Nt * d * 4, cudaMemcpyDeviceToHost, st));
   // host outputs: asynchronous like every other result (complete once `stream` reaches this point)
   CU(cudaGetLastError());
+  return STCA_OK;
+}
+
+// ===========================================================================
+// stca_profile: per-phase CUDA-event regions on the launching stream
+// ===========================================================================
+extern "C" stca_status stca_profile(stca_handle *h, int32_t enable) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  h->prof = enable != 0;
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_profile_read(stca_handle *h, double *ms, int64_t *count) {
+  if (!h || !ms || !count) return STCA_ERR_INVALID_ARG;
+  for (int p = 0; p < STCA_PH_N; ++p) {
+    ms[p] = 0.0;
+    count[p] = 0;
+  }
+  CU(cudaSetDevice(h->cfg.device));
+  for (ProfRegion &r : h->prof_open) {
+    CU(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.phase] += t;
+    count[r.phase] += 1;
+    h->prof_pool.push_back(r.a);
+    h->prof_pool.push_back(r.b);
+  }
+  h->prof_open.clear();
+  return STCA_OK;
+}
+
+// Stage-isolated test hook (not part of include/stca.h): during the next stca_forward, copy layer
+// `layer`'s reordered queries U [Nt h x d] (a3, pre-scaled by log2(e)/sqrt(d_h)) and the attention
+// output Y [Nt h x d] (a4 after the split-K fold) in the storage type into the caller's DEVICE
+// buffers, so a test can re-evaluate the softmax in f64 from the GPU's own bf16 operands.
+extern "C" stca_status stca_debug_capture(stca_handle *h, int32_t layer, void *U_out, void *Y_out) {
+  if (!h || !U_out || !Y_out || layer < 1 || layer > h->cfg.M) return STCA_ERR_INVALID_ARG;
+  h->cap_layer = layer;
+  h->cap_U = U_out;
+  h->cap_Y = Y_out;
   return STCA_OK;
 }

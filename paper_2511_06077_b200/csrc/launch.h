@@ -14,6 +14,14 @@ enum Epi { EPI_STORE = 0, EPI_SWIGLU = 1 };
 // process-wide count of kernels launched by libstca (stca_kernel_launches())
 void note_launch(int n = 1);
 
+// Per-device launch setup (cudaFuncSetAttribute applies to the CURRENT device's context only, so a
+// process-wide "done" flag would skip it for a handle on a second device).  Thread-safe, cached per
+// (kernel, device ordinal).
+cudaError_t smem_optin(const void *kernel, int bytes);   // MaxDynamicSharedMemorySize opt-in
+int sm_count();                                          // SMs of the current device
+// co-resident clusters of `cluster` CTAs of `kernel` (threads, smem) on the current device (>= 1)
+int cluster_occupancy(const void *kernel, int threads, int smem, int cluster);
+
 // Programmatic dependent launch for the forward's kernel chain: the kernel may be scheduled while
 // its predecessor in the stream drains, so its launch and prologue (barrier init, TMEM alloc,
 // tensor-map prefetch) overlap the predecessor's tail.  Every kernel launched this way executes

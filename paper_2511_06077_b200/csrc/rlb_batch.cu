@@ -1,7 +1,7 @@
 // rlb_batch.cu -- the training data path into the ragged forward:
-// stochastic train lengths (Eq. beta-scale, P:L255-260), temporal suffix (P:L275), global length
-// allocation against the budget B * L_avg (P:L281-283; DESIGN.md reading R-N2b) and sequence
-// compaction with its segment map and ragged index (P:L284-289).
+// stochastic train lengths (Eq. beta-scale, P:L255-260), temporal suffix (P:L279), global length
+// allocation against the budget B * L_avg (P:L286; DESIGN.md reading R-N2b) and sequence
+// compaction with its segment map and ragged index (P:L287-289).
 //
 // k_rlb_allocate: one CTA; B-sized integer work (reductions, O(B^2 / threads) ranking of the slack
 //   pass, scan).  Exact: int64 and unsigned __int128 for req_b * budget; the only floating-point
@@ -18,7 +18,6 @@
 
 namespace {
 
-__device__ int g_rlb_status;   // 0 ok, 1 infeasible budget, 2 s outside [0, 1]
 
 constexpr int kAllocThreads = 1024;
 constexpr int64_t kMaxB = 49152;   // 4 B of dynamic SMEM per sequence for the ranking
@@ -55,7 +54,8 @@ __global__ void __launch_bounds__(kAllocThreads) k_rlb_allocate(const double *__
                                                                  const int64_t *__restrict__ hist_off, int64_t B,
                                                                  int32_t L_min, int32_t L_max, int64_t budget,
                                                                  int64_t *__restrict__ alloc,
-                                                                 int64_t *__restrict__ new_off) {
+                                                                 int64_t *__restrict__ new_off,
+                                                                 int *__restrict__ status) {
   extern __shared__ int32_t trunc[];   // req_b - alloc_b if sequence b may take +8, else -1
   __shared__ int64_t s_total, s_slack;
   __shared__ int s_bad;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kAllocThreads) k_rlb_allocate(const double *__
   }
   if (threadIdx.x == 0) {
     new_off[B] = carry;
-    g_rlb_status = s_bad;
+    *status = s_bad;  // 0 ok, 1 infeasible budget, 2 s outside [0, 1] (this call's own word)
   }
 }
 
@@ -225,14 +225,24 @@ extern "C" stca_status stca_rlb_allocate(const double *s, const int64_t *hist_of
     return STCA_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t smem = (size_t)B * sizeof(int32_t);
-  if (cudaFuncSetAttribute(k_rlb_allocate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return STCA_ERR_CUDA;
-  k_rlb_allocate<<<1, kAllocThreads, smem, st>>>(s, hist_off, B, L_min, L_max, (int64_t)B * L_avg, alloc, new_off);
+  if (stca::smem_optin((const void *)k_rlb_allocate, (int)smem) != cudaSuccess) return STCA_ERR_CUDA;
+  int *dstatus = nullptr;  // this call's status word (stream-ordered), never shared with another call
+  if (cudaMallocAsync(&dstatus, sizeof(int), st) != cudaSuccess) {
+    cudaGetLastError();
+    return STCA_ERR_OOM;
+  }
+  k_rlb_allocate<<<1, kAllocThreads, smem, st>>>(s, hist_off, B, L_min, L_max, (int64_t)B * L_avg, alloc, new_off,
+                                                 dstatus);
   stca::note_launch();
+  const cudaError_t le = cudaGetLastError();
   int status = 0;
-  if (cudaMemcpyFromSymbolAsync(&status, g_rlb_status, sizeof(int), 0, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess)
+  const bool ok = le == cudaSuccess &&
+                  cudaMemcpyAsync(&status, dstatus, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess;
+  cudaFreeAsync(dstatus, st);
+  if (!ok || cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaGetLastError();
     return STCA_ERR_CUDA;
+  }
   return status ? STCA_ERR_INVALID_ARG : STCA_OK;
 }
 
@@ -245,7 +255,7 @@ extern "C" stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const 
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t cpr = row_bytes / 16;
   const int cpr_log2 = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
-  k_rlb_gather<<<4 * 148 + 1, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, cpr, cpr_log2,
+  k_rlb_gather<<<4 * stca::sm_count() + 1, kGatherThreads, 0, st>>>((const uint4 *)X, hist_off, alloc, new_off, B, cpr, cpr_log2,
                                                        L_avg, seg_off, segs, (uint4 *)P);
   stca::note_launch(1);
   return cudaGetLastError() == cudaSuccess ? STCA_OK : STCA_ERR_CUDA;

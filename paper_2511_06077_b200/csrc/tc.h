@@ -30,6 +30,10 @@ struct TcProj {
   const float *g[16] = {}, *b[16] = {};
   void *out = nullptr;            // layer i at out + i * out_layer_stride elements (bf16)
   int64_t out_layer_stride = 0;
+  // two-GEMM path (d != 128): caller-owned H scratch of H_rows x rd bf16 (rows are processed in
+  // pieces of at most H_rows)
+  void *H = nullptr;
+  int64_t H_rows = 0;
   // fused kernel (d == 128): all layers concatenated
   const void *W1cat = nullptr;    // [M x 2rd x d] bf16, per layer the chunk-interleaved W1^T
   const void *Wocat = nullptr;    // [M x rd x d] bf16, row-major W_o (MN-major B operand)
@@ -51,10 +55,11 @@ bool tc_prepare_ffn(const float *Wu, const float *Wv, const float *Wo, int d, in
 bool tc_prepare_layer(const void *WQK, const void *WVO, const void *WC, int i, int d, int h, TcWeights *tc,
                       const DevAlloc &alloc);
 cudaError_t tc_project(const TcProj &p, cudaStream_t st);
-// SwiGLUFFN (+LN if g) over rows; outputs bf16 (out_s, ldo) and/or fp32 (out_f, ldof)
+// SwiGLUFFN (+LN if g) over rows; outputs bf16 (out_s, ldo) and/or fp32 (out_f, ldof).  H: caller-owned
+// scratch of at least rows * rd bf16 (the handle's, so concurrent handles / streams never share it)
 cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, const void *Wo, int d, int rd,
                    const float *g, const float *b, float eps, void *out_s, int64_t ldo, float *out_f, int64_t ldof,
-                   cudaStream_t st);
+                   void *H, cudaStream_t st);
 // C[M x N] = A[M x K] (bf16, lda) . B where Bt = B^T [N x K] bf16 K-major
 cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
                     float *Cf, int64_t ldcf, cudaStream_t st);

@@ -401,16 +401,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }  // namespace tc
 
 bool tc_attention_supported(int d) { return d == tc::AT_D; }
-int tc_attention_ctas() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 1;
-  }
-  return n;
-}
+int tc_attention_ctas() { return sm_count(); }
 
 cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                          const int32_t *cta_off, const int32_t *cta_items, int n_ctas, int d, void *Y, float *part,
@@ -420,12 +411,8 @@ cudaError_t tc_attention(const void *U, int64_t NQ, const void *Xt, int64_t T2, 
   CUtensorMap mx, mu;
   if (!tc::make_map_bf16(&mx, Xt, T2, d, d, 128) || !tc::make_map_bf16(&mu, U, NQ, d, d, 128))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_tc_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::AT_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e0 = smem_optin((const void *)tc::k_tc_attention, tc::AT_SMEM);
+  if (e0 != cudaSuccess) return e0;
   unsigned long long *trace = nullptr;
   const char *trace_path = getenv("STCA_TRACE_ATTN");  // debug only: clock64 stamps of CTA 0
   if (trace_path && cudaMalloc(&trace, 8192 * 8) == cudaSuccess) cudaMemsetAsync(trace, 0, 8192 * 8, st);

@@ -340,12 +340,8 @@ cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64
   CUtensorMap mx, mu;
   if (!tc::make_map_bf16(&mx, Xt, T2, C::D, C::D, C::BK) || !tc::make_map_bf16(&mu, U, NQ, C::D, C::D, C::NQ))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_tc_attention_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e0 = smem_optin((const void *)tc::k_tc_attention_narrow, C::SMEM);
+  if (e0 != cudaSuccess) return e0;
   note_launch();
   return launch_pdl(tc::k_tc_attention_narrow, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx, mu,
                     items, cta_off, cta_items, (bf16 *)Y, part);

@@ -297,13 +297,8 @@ cudaError_t tc_attention_wide(const void *U, int64_t NQ, const void *Xt, int64_t
   if (!tc::make_map_bf16(&mx, Xt, T2, d, d, 64)) return cudaErrorInvalidValue;
 #define WLAUNCH(DD)                                                                                              \
   {                                                                                                              \
-    static bool attr = false;                                                                                    \
-    if (!attr) {                                                                                                 \
-      cudaError_t e = cudaFuncSetAttribute(tc::k_tc_attention_wide<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           tc::WCfg<DD>::SMEM);                                                  \
-      if (e != cudaSuccess) return e;                                                                            \
-      attr = true;                                                                                               \
-    }                                                                                                            \
+    cudaError_t e0 = smem_optin((const void *)tc::k_tc_attention_wide<DD>, tc::WCfg<DD>::SMEM);                 \
+    if (e0 != cudaSuccess) return e0;                                                                            \
     note_launch();                                                                                               \
     tc::k_tc_attention_wide<DD><<<(unsigned)n_items, 352, tc::WCfg<DD>::SMEM, st>>>(mx, (const bf16 *)U, NQ, items, \
                                                                                      (bf16 *)Y, part);           \

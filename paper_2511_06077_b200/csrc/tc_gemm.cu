@@ -388,33 +388,9 @@ static cudaError_t launch_gemm(const void *A, int64_t lda, const void *Bt, int64
   using C = GemmCfg<BN>;
   CUtensorMap ma, mb;
   if (!make_map_bf16(&ma, A, M, K, lda, 128) || !make_map_bf16(&mb, Bt, N, K, K, C::NS / 2)) return cudaErrorInvalidValue;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  static int mc = 0;  // co-resident 2-CTA clusters of this instantiation
-  if (!mc) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2);
-    cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cudaLaunchAttribute ca[1];
-    ca[0].id = cudaLaunchAttributeClusterDimension;
-    ca[0].val.clusterDim.x = 2;
-    ca[0].val.clusterDim.y = 1;
-    ca[0].val.clusterDim.z = 1;
-    cfg.attrs = ca;
-    cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&mc, (const void *)k_tc_gemm<BN, EPI>, &cfg) != cudaSuccess || mc <= 0) {
-      cudaGetLastError();
-      int dev = 0, nsm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      mc = nsm > 1 ? nsm / 2 : 1;
-    }
-  }
+  cudaError_t e0 = smem_optin((const void *)k_tc_gemm<BN, EPI>, C::SMEM);
+  if (e0 != cudaSuccess) return e0;
+  const int mc = cluster_occupancy((const void *)k_tc_gemm<BN, EPI>, GEMM_THREADS, C::SMEM, 2);  // co-resident pairs
   const int64_t npairs = ((M + 127) / 128 + 1) / 2 * (N / BN);
   note_launch();
   cudaLaunchConfig_t cfg = {};
@@ -472,32 +448,13 @@ cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N
   return gemm_dispatch(tc::TEPI_STORE, A, lda, Bt, M, N, K, ea, st);
 }
 
-// ---- SwiGLUFFN (+LN) over rows, as two tcgen05 GEMMs with H (bf16) in a scratch buffer ----
-static void *g_hscratch = nullptr;
-static size_t g_hcap = 0;
-static std::mutex g_hmu;
-
-static cudaError_t hscratch(size_t bytes, void **out) {
-  std::lock_guard<std::mutex> lk(g_hmu);
-  if (bytes > g_hcap) {
-    if (g_hscratch) cudaFree(g_hscratch);
-    g_hscratch = nullptr;
-    g_hcap = 0;
-    cudaError_t e = cudaMalloc(&g_hscratch, bytes);
-    if (e != cudaSuccess) return e;
-    g_hcap = bytes;
-  }
-  *out = g_hscratch;
-  return cudaSuccess;
-}
-
+// ---- SwiGLUFFN (+LN) over rows, as two tcgen05 GEMMs with H (bf16) in the caller's scratch ----
 cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, const void *Wo, int d, int rd,
                    const float *g, const float *b, float eps, void *out_s, int64_t ldo, float *out_f, int64_t ldof,
-                   cudaStream_t st) {
+                   void *H, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  void *H = nullptr;
-  cudaError_t e = hscratch((size_t)rows * rd * 2, &H);
-  if (e != cudaSuccess) return e;
+  if (!H) return cudaErrorInvalidValue;
+  cudaError_t e;
   tc::EpiArgs e1{(bf16 *)H, rd, nullptr, 0, nullptr, nullptr, 0.f};
   e = gemm_dispatch(tc::TEPI_SWIGLU, in, ldi, W1, rows, 2 * rd, d, e1, st);
   if (e != cudaSuccess) return e;

@@ -2,6 +2,9 @@
 // and the history projection driver of the bf16 path.
 #include <string.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "launch.h"
@@ -40,17 +43,83 @@ static uint16_t to_bf16_bits(float f) {
   return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
 }
 
-bool tc_available() {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0, major = 0, minor = 0;
-    ok = cudaGetDevice(&dev) == cudaSuccess &&
-         cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
-         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess && major == 10 &&
-         minor == 0;
+// ---- per-device caches (every entry keyed by the current device ordinal) ----
+static std::mutex g_dev_mu;
+static std::map<std::pair<const void *, int>, int> g_optin, g_occ;
+static std::map<int, int> g_sms, g_tc_ok;
+
+static int cur_dev() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
+    dev = 0;
   }
-  return ok == 1;
+  return dev;
+}
+
+cudaError_t smem_optin(const void *kernel, int bytes) {
+  const int dev = cur_dev();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  int &done = g_optin[{kernel, dev}];
+  if (done >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done = bytes;
+  return e;
+}
+
+int sm_count() {
+  const int dev = cur_dev();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  int &n = g_sms[dev];
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 1;
+    }
+  }
+  return n;
+}
+
+int cluster_occupancy(const void *kernel, int threads, int smem, int cluster) {
+  const int dev = cur_dev();
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_occ.find({kernel, dev});
+    if (it != g_occ.end()) return it->second;
+  }
+  int mc = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cluster);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute ca[1];
+  ca[0].id = cudaLaunchAttributeClusterDimension;
+  ca[0].val.clusterDim.x = (unsigned)cluster;
+  ca[0].val.clusterDim.y = 1;
+  ca[0].val.clusterDim.z = 1;
+  cfg.attrs = ca;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&mc, kernel, &cfg) != cudaSuccess || mc <= 0) {
+    cudaGetLastError();
+    mc = std::max(1, sm_count() / cluster);
+  }
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_occ[{kernel, dev}] = mc;
+  return mc;
+}
+
+bool tc_available() {
+  const int dev = cur_dev();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_tc_ok.find(dev);
+  if (it != g_tc_ok.end()) return it->second == 1;
+  int major = 0, minor = 0;
+  const bool ok = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+                  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess &&
+                  major == 10 && minor == 0;
+  cudaGetLastError();
+  g_tc_ok[dev] = ok ? 1 : 0;
+  return ok;
 }
 
 bool tc_prepare_ffn(const float *Wu, const float *Wv, const float *Wo, int d, int rd, TcWeights *tc,

@@ -509,25 +509,10 @@ cudaError_t tc_project(const TcProj &p, cudaStream_t st) {
         !tc::make_map_bf16(&mx, p.X, p.rows, p.d, p.d, tc::PJ_ROWS))
       return cudaErrorInvalidValue;
     auto kern = tc::k_tc_project;
-    static int mc = 0;
-    if (mc == 0) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PJ_SMEM);
-      if (e != cudaSuccess) return e;
-      // persistent grid: as many 2-CTA clusters as can be co-resident (1 CTA per SM)
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(2, 1, 1);
-      cfg.blockDim = dim3(tc::PJ_THREADS, 1, 1);
-      cfg.dynamicSmemBytes = tc::PJ_SMEM;
-      cfg.stream = st;
-      e = cudaOccupancyMaxActiveClusters(&mc, (const void *)kern, &cfg);
-      if (e != cudaSuccess || mc <= 0) {
-        int dev = 0, nsm = 0;
-        cudaGetLastError();
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        mc = std::max(1, nsm / 2);
-      }
-    }
+    cudaError_t e0 = smem_optin((const void *)kern, tc::PJ_SMEM);
+    if (e0 != cudaSuccess) return e0;
+    // persistent grid: as many 2-CTA clusters as can be co-resident (1 CTA per SM)
+    const int mc = cluster_occupancy((const void *)kern, tc::PJ_THREADS, tc::PJ_SMEM, 2);
     const int64_t tiles = (p.rows + tc::PJ_ROWS - 1) / tc::PJ_ROWS;
     const int npairs = (int)((tiles + 1) / 2);
     tc::ProjArgs a{(const bf16 *)p.X, p.rows, p.gcat, p.bcat, p.M, p.rd / tc::PJ_NCH, npairs, p.eps, nullptr};
@@ -548,13 +533,14 @@ cudaError_t tc_project(const TcProj &p, cudaStream_t st) {
     return cudaGetLastError();
   }
   // other widths: per layer, two tcgen05 GEMMs (SwiGLU epilogue -> H bf16, then W_o + LN epilogue)
-  const int64_t R = 1 << 18;
+  const int64_t R = p.H_rows;
+  if (!p.H || R <= 0) return cudaErrorInvalidValue;
   for (int i = 0; i < p.M; ++i) {
     for (int64_t r0 = 0; r0 < p.rows; r0 += R) {
       const int64_t rows = std::min<int64_t>(R, p.rows - r0);
       const bf16 *x = (const bf16 *)p.X + r0 * p.d;
       bf16 *out = (bf16 *)p.out + (int64_t)i * p.out_layer_stride + r0 * p.d;
-      cudaError_t e = tc_ffn(x, p.d, rows, p.W1[i], p.Wo[i], p.d, p.rd, p.g[i], p.b[i], p.eps, out, p.d, nullptr, 0, st);
+      cudaError_t e = tc_ffn(x, p.d, rows, p.W1[i], p.Wo[i], p.d, p.rd, p.g[i], p.b[i], p.eps, out, p.d, nullptr, 0, p.H, st);
       if (e != cudaSuccess) return e;
     }
   }

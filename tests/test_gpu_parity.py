@@ -190,10 +190,82 @@ def test_full_size_sampled(name):
     assert np.isfinite(Z).all() and np.isfinite(z).all()
 
 
+def _run_bits(wl, chunk_keys=0):
+    """run_gpu for a bits_only workload (the multi-GB full-size configs): device inputs from the bits."""
+    import torch
+    import paper_2511_06077_b200 as stca
+    c = wl.cfg
+    m = stca.STCA(workload.full_weights(wl), d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, dtype=c.dtype,
+                  with_z=c.with_z, chunk_keys=chunk_keys)
+    X = torch.from_numpy(wl.X_bits.view(np.int16)).cuda()
+    xt = torch.from_numpy(wl.xt_bits.view(np.int16)).cuda()
+    Z = torch.full((wl.Nt, c.M, c.d), float("nan"), device="cuda")
+    z = torch.full((wl.Nt, c.d), float("nan"), device="cuda")
+    m.project_history(X, wl.hist_off)
+    m.forward(xt, wl.tgt_off, Z, z)
+    torch.cuda.synchronize()
+    m.close()
+    return Z, z
+
+
+def _check_sample(wl, Z, z, sample, tol):
+    """The oracle on the sampled requests only (requests are independent)."""
+    sub = workload.subset(wl, sample)
+    Zr, zr, _ = oracle.forward_workload(sub, nthreads=8)
+    rows = np.concatenate([np.arange(wl.tgt_off[b], wl.tgt_off[b + 1]) for b in sample])
+    Zg, zg = Z[rows].cpu().double().numpy(), z[rows].cpu().double().numpy()
+    assert np.isfinite(Zg).all() and np.isfinite(zg).all()
+    eZ, ez = rowrel(Zg, Zr), rowrel(zg, zr)
+    assert eZ.max() <= tol, (eZ.max(), np.unravel_index(eZ.argmax(), eZ.shape))
+    assert ez.max() <= tol, ez.max()
+    assert not torch_isnan_any(Z) and not torch_isnan_any(z)
+
+
+def torch_isnan_any(t):
+    return bool(t.isnan().any())
+
+
+def test_full_size_multi_sampled():
+    """The multi config at full size (8192 requests, ragged avg 2k / max 10k, m = 8: the transposed
+    narrow kernel), in the bench's single-GPU launch configuration; oracle on shortest, longest, first
+    and median-length requests."""
+    wl = workload.make_workload("multi", seed=0, bits_only=True)
+    Z, z = _run_bits(wl)
+    L = wl.lengths
+    sample = sorted({0, int(np.argmin(L)), int(np.argmax(L)), int(np.argsort(L)[len(L) // 2])})
+    _check_sample(wl, Z, z, sample, TOL["bf16"])
+
+
+def test_full_size_capacity_sampled():
+    """The capacity config at full size (512 requests, d = 512, h = 8, M = 8, m = 32: the wide kernel and
+    the 2-GEMM projection), bench launch configuration; the f64 oracle checks the shortest request, the
+    one closest to 1000 keys and the first request whose history is at most 2000 keys (a 10k d = 512
+    history costs the scalar oracle minutes; long histories are covered at this shape by
+    test_capacity_shape_d512_sampled)."""
+    wl = workload.make_workload("capacity", seed=0, bits_only=True)
+    Z, z = _run_bits(wl)
+    L = wl.lengths
+    sample = sorted({int(np.argmin(L)), int(np.argmin(np.abs(L - 1000))), int(np.nonzero(L <= 2000)[0][0])})
+    _check_sample(wl, Z, z, sample, TOL["bf16"])
+
+
+def test_persistent_attention_more_than_128_items_per_cta():
+    """k_tc_attention caches a CTA's first AT_MAXI = 128 work items in shared memory and reads later ones
+    from global memory: 19200 single-tile requests with m_b h = 68 query rows (the 128-row kernel) give
+    every CTA of the 148-CTA grid about 130 items; the sample covers items beyond the 128th."""
+    rng = np.random.default_rng(7)
+    B = 19200
+    lengths = rng.integers(1, 129, size=B)
+    cfg = make_cfg(B=B, m=17, M=2)
+    wl = workload.make_workload(cfg, seed=9, lengths=lengths)
+    Z, z = _run_bits(wl)
+    _check_sample(wl, Z, z, [0, 147, 18943, 18944, 19000, 19199], TOL["bf16"])
+
+
 def test_capacity_shape_d512_sampled():
     """BASELINE capacity config shape (d = 512, h = 8, M = 8, 32 targets per request), a few ragged
     requests up to L = 10k: the 2-GEMM tcgen05 projection (LayerNorm over a 512-wide TMEM row) and
-    the CUDA-core attention sweep."""
+    the wide tcgen05 attention kernel."""
     cfg = workload.CONFIGS["capacity"]
     wl = workload.make_workload(cfg, seed=2, B=4, lengths=np.array([10000, 64, 1500, 4104]))
     Z, z = run_gpu(wl)

@@ -115,3 +115,71 @@ def test_degenerate_batches():
     Z, z = run_gpu(wl1)
     Zr, zr, rows = oracle.forward_workload(wl1, nthreads=2)
     assert rowrel(Z[rows], Zr).max() <= 2e-2 and rowrel(z[rows], zr).max() <= 2e-2
+
+
+def _f64_attention(U, Xc, hist_len, tgt_off, h):
+    """f64 reference of a4 on the GPU's own operands: for each query row u (log2 domain, pre-scaled by
+    log2(e)/sqrt(d_h)) of request b, alpha = 2^(u X~_b^T) / sum, y = alpha X~_b (Eq.(13)).
+    Also returns A = alpha |X~_b| (elementwise), the scale of every rounding error below."""
+    Y = np.zeros_like(U)
+    A = np.zeros_like(U)
+    k0 = 0
+    for b in range(len(hist_len)):
+        Xb = Xc[k0:k0 + hist_len[b]]
+        k0 += hist_len[b]
+        q0, q1 = tgt_off[b] * h, tgt_off[b + 1] * h
+        if q1 == q0:
+            continue
+        s = U[q0:q1] @ Xb.T
+        p = np.exp2(s - s.max(1, keepdims=True))
+        alpha = p / p.sum(1, keepdims=True)
+        Y[q0:q1] = alpha @ Xb
+        A[q0:q1] = alpha @ np.abs(Xb)
+    return Y, A
+
+
+# K-C stage bound, derived from the kernel's arithmetic (DESIGN.md §8): y_gpu = sum_j bf16(p_j) x_j / l
+# with the sum l of the unrounded fp32 p_j, so rounding P to bf16 (relative 2^-9 per weight) moves y_e
+# by at most 2^-9 A_e, A_e = sum_j alpha_j |x_je|; a split-K partial is stored as bf16(O/l) (another
+# 2^-9 A_e after the fold's convex combination) and Y itself is rounded to bf16 (2^-9 |y_e| <= 2^-9 A_e);
+# the exponentials (MUFU ex2.approx and the FMA-pipe cubic, relative error <= 1e-4, in the numerator
+# and the sum) add <= 2e-4 A_e.  fp32 accumulation of S and of the sums is negligible at these sizes.
+KC_BOUND = 3 * 2.0 ** -9 + 4e-4
+
+
+@pytest.mark.parametrize("d,h,m,wq", [(128, 4, 16, 1.0), (128, 4, 64, 1.0), (128, 4, 8, 8.0), (128, 4, 64, 8.0),
+                                      (256, 8, 32, 1.0), (512, 8, 32, 1.0)])
+def test_attention_stage_isolated(d, h, m, wq):
+    """the attention output Y of one layer against an f64 softmax over the GPU's own
+    bf16 U and X~ (read back from the device), elementwise within the arithmetic's rounding bound
+    KC_BOUND * A_e (the SURVEY's proposed 4e-3 row-relative bound is below the two bf16 output roundings
+    the kernels do: measured 4.4-6.4e-3 row-relative; row-relative <= 1e-2 is kept as a second check).  m h <= 64 takes the
+    transposed kernel, 256 the 128-row kernel, d = 256 / 512 the wide kernel; the 9000-key history
+    is split into chunks and folded (split-K LSE merge); wq = 8 is the sharp-softmax regime."""
+    import torch
+    import paper_2511_06077_b200 as stca
+    lengths = np.array([9000, 1, 333, 2049])
+    cfg = make_cfg(B=len(lengths), m=m, d=d, h=h, M=2)
+    wl = workload.make_workload(cfg, seed=21, lengths=lengths, wq_scale=wq)
+    c = wl.cfg
+    mdl = stca.STCA(workload.full_weights(wl), d=d, h=h, r=c.r, M=c.M, dtype="bf16")
+    X, xt = device_inputs(wl)
+    NQ = wl.Nt * h
+    Ucap = torch.zeros(NQ, d, dtype=torch.int16, device="cuda")
+    Ycap = torch.zeros(NQ, d, dtype=torch.int16, device="cuda")
+    Z = torch.empty(wl.Nt, c.M, d, device="cuda")
+    for layer in (1, 2):
+        mdl.project_history(X, wl.hist_off)
+        mdl.debug_capture(layer, Ucap, Ycap)
+        mdl.forward(xt, wl.tgt_off, Z, None)
+        torch.cuda.synchronize()
+        U = workload.bits_to_f32(Ucap.cpu().numpy().view(np.uint16)).reshape(NQ, d).astype(np.float64)
+        Yg = workload.bits_to_f32(Ycap.cpu().numpy().view(np.uint16)).reshape(NQ, d).astype(np.float64)
+        Xc = mdl.read_cache(layer, 0, int(lengths.sum())).astype(np.float64)
+        ref, A = _f64_attention(U, Xc, lengths, wl.tgt_off, h)
+        assert np.isfinite(Yg).all()
+        ratio = np.abs(Yg - ref) / (KC_BOUND * A + 1e-30)
+        assert ratio.max() <= 1.0, (layer, ratio.max(), np.unravel_index(ratio.argmax(), ratio.shape))
+        e = rowrel(Yg, ref)
+        assert e.max() <= 1e-2, (layer, e.max(), int(e.argmax()))
+    mdl.close()

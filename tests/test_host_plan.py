@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for s in sorted(declared):
         assert hasattr(L, s), s
     assert set(_lib.SYMBOLS) == declared
-    assert L.stca_abi_version() == 1
+    assert L.stca_abi_version() == 2
 
 
 def test_status_strings():

@@ -28,12 +28,16 @@ def _worker(rank, world, port, q):
         import paper_2511_06077_b200 as stca
         out = {}
         # PAR1: every rank computes the same LPT plan from the global request list, independently
-        wl = workload.make_workload("multi", seed=3, B=512)
-        c = wl.cfg
-        L = np.minimum(wl.lengths, c.L_infer)
-        m = np.diff(wl.tgt_off)
-        cost = L * (6 * c.r * c.d * c.d * c.M) + m * L * (4 * c.h * c.d * c.M)
+        import bench
+        wl = workload.make_workload("multi", seed=3, B=512, bits_only=True)
+        cost = bench.request_cost(wl)
         plan = torch.from_numpy(stca.plan_shards(cost, world).astype(np.int64))
+        # bench.py's shard extraction on this rank: requests, offsets and rows, hashed for the parent
+        mine_b = bench.shard_requests(wl, world, rank)
+        sh = workload.subset(wl, mine_b, with_f32=False)
+        import hashlib
+        out["shard"] = (mine_b.tolist(), hashlib.sha256(sh.X_bits.tobytes()).hexdigest(),
+                        hashlib.sha256(sh.xt_bits.tobytes()).hexdigest(), sh.hist_off.tolist(), sh.tgt_off.tolist())
         plans = [torch.zeros_like(plan) for _ in range(world)]
         dist.all_gather(plans, plan)
         out["plans_equal"] = all(torch.equal(p, plans[0]) for p in plans)
@@ -72,5 +76,23 @@ def test_two_ranks_gloo():
         assert p.exitcode == 0
     res = dict(q.get() for _ in range(world))
     for r in range(world):
-        assert res[r]["plans_equal"] and res[r]["covered"] and res[r]["merge_sources_ok"], res[r]
-        assert res[r]["balance"] < 1.05, res[r]
+        ok = {k: v for k, v in res[r].items() if k != "shard"}
+        assert res[r]["plans_equal"] and res[r]["covered"] and res[r]["merge_sources_ok"], ok
+        assert res[r]["balance"] < 1.05, ok
+    # the ranks' shards equal a single-process split bit for bit, and together cover every request once
+    import hashlib
+    import bench
+    wl = workload.make_workload("multi", seed=3, B=512)
+    seen = []
+    for r in range(world):
+        reqs, hx, ht, hoff, toff = res[r]["shard"]
+        assert reqs == sorted(reqs)
+        seen += reqs
+        rows = np.concatenate([np.arange(wl.hist_off[b], wl.hist_off[b + 1]) for b in reqs])
+        trows = np.concatenate([np.arange(wl.tgt_off[b], wl.tgt_off[b + 1]) for b in reqs])
+        assert hashlib.sha256(np.ascontiguousarray(wl.X_bits[rows]).tobytes()).hexdigest() == hx
+        assert hashlib.sha256(np.ascontiguousarray(wl.xt_bits[trows]).tobytes()).hexdigest() == ht
+        assert hoff == np.concatenate([[0], np.cumsum(wl.lengths[reqs])]).tolist()
+        assert toff == np.concatenate([[0], np.cumsum(np.diff(wl.tgt_off)[reqs])]).tolist()
+        assert list(bench.shard_requests(wl, world, r)) == reqs
+    assert sorted(seen) == list(range(len(wl.lengths)))

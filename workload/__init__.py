@@ -196,10 +196,22 @@ def _normal_rows(rng: np.random.Generator, rows: int, d: int, chunk_rows: int = 
     return out
 
 
+def _normal_rows_bits(rng: np.random.Generator, rows: int, d: int, chunk_rows: int = 1 << 16) -> np.ndarray:
+    """The same draws as _normal_rows, kept only as bf16 bit patterns (chunk by chunk: no float32 copy
+    of the whole matrix is ever held)."""
+    out = np.empty((rows, d), dtype=np.uint16)
+    for s in range(0, rows, chunk_rows):
+        e = min(rows, s + chunk_rows)
+        out[s:e] = bf16_bits(rng.standard_normal((e - s, d), dtype=np.float32)).reshape(e - s, d)
+    return out
+
+
 def make_workload(cfg, seed: int = 0, B: Optional[int] = None, *, ln_affine: bool = False,
                   wq_scale: float = 1.0, lengths: Optional[np.ndarray] = None,
-                  m: Optional[int] = None) -> Workload:
-    """Draw one workload.  ``B``/``m``/``lengths`` override the config (tests)."""
+                  m: Optional[int] = None, bits_only: bool = False) -> Workload:
+    """Draw one workload.  ``B``/``m``/``lengths`` override the config (tests).  ``bits_only`` (bf16
+    configs): keep X only as bf16 bit patterns (``X`` is None; ``subset`` widens the rows it needs),
+    for the multi-GB bench workloads.  The draws are identical either way."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     B = cfg.B if B is None else int(B)
@@ -231,6 +243,12 @@ def make_workload(cfg, seed: int = 0, B: Optional[int] = None, *, ln_affine: boo
     tgt_off = np.arange(B + 1, dtype=np.int64) * m
     T, Nt = int(hist_off[-1]), int(tgt_off[-1])
 
+    if bf16 and bits_only:
+        X_bits = _normal_rows_bits(rng, T, cfg.d)
+        xt_bits = _normal_rows_bits(rng, Nt, cfg.d)
+        return Workload(cfg=cfg, seed=seed, weights=weights, lengths=lengths, hist_off=hist_off,
+                        tgt_off=tgt_off, X=None, xt=bits_to_f32(xt_bits).reshape(Nt, cfg.d), X_bits=X_bits,
+                        xt_bits=xt_bits)
     X = _normal_rows(rng, T, cfg.d)
     xt = _normal_rows(rng, Nt, cfg.d)
     X_bits = xt_bits = None
@@ -261,3 +279,32 @@ def full_weights(wl: Workload) -> Dict[str, np.ndarray]:
     for k, v in weight_aliases(wl.cfg).items():
         w[k] = wl.weights[v]
     return w
+
+
+def subset(wl: Workload, requests, with_f32: bool = True) -> Workload:
+    """The workload restricted to ``requests`` (in the given order): their history rows and target
+    rows back to back, offsets rebuilt.  Pure row selection (a request shard of a data-parallel rank,
+    or the oracle's sample); no arithmetic."""
+    req = np.asarray(requests, dtype=np.int64)
+    L = wl.lengths[req]
+    m = np.diff(wl.tgt_off)[req]
+    hist_off = np.zeros(len(req) + 1, dtype=np.int64)
+    np.cumsum(L, out=hist_off[1:])
+    tgt_off = np.zeros(len(req) + 1, dtype=np.int64)
+    np.cumsum(m, out=tgt_off[1:])
+
+    def rows(off, idx):
+        if len(idx) == 0:
+            return np.zeros(0, dtype=np.int64)
+        return np.concatenate([np.arange(off[b], off[b + 1], dtype=np.int64) for b in idx])
+    hr, tr = rows(wl.hist_off, req), rows(wl.tgt_off, req)
+    d = wl.cfg.d
+    X_bits = wl.X_bits[hr] if wl.X_bits is not None else None
+    xt_bits = wl.xt_bits[tr] if wl.xt_bits is not None else None
+    if X_bits is not None:
+        X = bits_to_f32(X_bits).reshape(-1, d) if with_f32 else None
+        xt = bits_to_f32(xt_bits).reshape(-1, d)
+    else:
+        X, xt = wl.X[hr], wl.xt[tr]
+    return Workload(cfg=wl.cfg, seed=wl.seed, weights=wl.weights, lengths=L, hist_off=hist_off, tgt_off=tgt_off,
+                    X=X, xt=xt, X_bits=X_bits, xt_bits=xt_bits)
