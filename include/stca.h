@@ -139,6 +139,28 @@ stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const
 stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                          float *out_Z, float *out_z, void *stream);
 
+/* ---- session sharing: RLB extended across requests of the same user ----
+ * PAPER.md P:L45 ("can be extended to share across multiple requests for the same user/session") and
+ * P:L51 ("multi-request sharing for the same user/session").  stca_session_open gives the handle a
+ * persistent X~ cache of `capacity_rows` history rows per layer (M x capacity x d, storage dtype) and
+ * forgets any earlier projection.  stca_project_history_session then does what stca_project_history
+ * does for B requests of users user_id[b] (HOST int64 [B]) whose history has generation gen[b] (HOST
+ * int64 [B]; any caller value that changes whenever the user's kept rows change, e.g. the newest
+ * event's timestamp) -- except that a request whose (user, generation, kept length L'_b) is cached is
+ * not projected again: the following stca_forward calls attend over the cached rows, which are the
+ * same bits a fresh projection writes (the projection is row-wise).  The missing users' suffix rows
+ * are projected into one contiguous range of a FIFO ring; entries it overlaps are forgotten (if that
+ * would drop a hit of this batch, the cache is reset and the batch projected whole).  X, T and
+ * hist_off as in stca_project_history (every request's rows are passed; rows of hits are not read).
+ * *n_projected (may be NULL) = users projected by this call.  STATE before stca_session_open;
+ * INVALID_ARG for a user twice in one batch with different histories; OOM when the batch's new rows
+ * exceed the capacity; UNSUPPORTED in split-history mode.  A plain stca_project_history closes the
+ * session. */
+stca_status stca_session_open(stca_handle *h, int64_t capacity_rows, void *stream);
+stca_status stca_project_history_session(stca_handle *h, const int64_t *user_id, const int64_t *gen, const void *X,
+                                         int64_t T, const int64_t *hist_off, int64_t B, int64_t *n_projected,
+                                         void *stream);
+
 /* The projected history cache of the last stca_project_history, Eq.(2): rows [row0, row0 + nrows)
  * of X~(layer), layer = 1..M, in compacted cache order (request b's kept rows start at the sum of
  * the kept lengths L'_{b'} of the requests before it), widened to float32 into out [nrows x d]
@@ -154,9 +176,14 @@ stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t row0, int64_t
  * STCA_PH_FORWARD (a whole stca_forward).  Events between kernels remove the programmatic-
  * dependent-launch overlap across them, so profiled phase times are upper bounds of unprofiled
  * ones.  stca_profile_read waits for the recorded events, writes the total milliseconds and the
- * region count of every phase since the last read (arrays of STCA_PH_N) and resets. */
+ * region count of every phase since the last read (arrays of STCA_PH_N) and resets.
+ * `enable` is a bit mask: STCA_PROF_EVENTS (the regions above), STCA_PROF_TWICE_ATTENTION (every a4
+ * launch is issued twice: identical results, so the step-time difference over a timed region is
+ * the attention launches' marginal duration inside the real, PDL-overlapped pipeline) and
+ * STCA_PROF_TWICE_PROJECT (the same for the a1 projection launch). */
 enum { STCA_PH_PROJECT = 0, STCA_PH_ATTENTION = 1, STCA_PH_MERGE = 2, STCA_PH_TARGET = 3, STCA_PH_FORWARD = 4,
        STCA_PH_N = 5 };
+enum { STCA_PROF_EVENTS = 1, STCA_PROF_TWICE_ATTENTION = 2, STCA_PROF_TWICE_PROJECT = 4 };
 stca_status stca_profile(stca_handle *h, int32_t enable);
 stca_status stca_profile_read(stca_handle *h, double *ms, int64_t *count);
 
@@ -227,6 +254,38 @@ stca_status stca_rlb_allocate(const double *s, const int64_t *hist_off, int64_t 
 stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const int64_t *hist_off, const int64_t *alloc,
                              const int64_t *new_off, int64_t B, int32_t L_avg, void *P, int64_t *seg_off,
                              int64_t *segs, void *stream);
+
+/* ---- input-encoding prologue ----
+ * PAPER.md §3.1.1 "Input encoding" (video, action-type and position embeddings fused into x_j)
+ * and the time-delta side information (request time minus item timestamp); additive fusion as
+ * in SPEC S:L130-138.  Every pointer below is DEVICE memory owned by the caller (the struct itself is
+ * host memory), tables row-major in the storage dtype (bf16 bit patterns or fp32), 16-byte aligned:
+ *   video    [n_video + 1 x d]   row n_video: every id outside [0, n_video) (out of vocabulary)
+ *   action   [n_action + 1 x d]  row n_action: out of vocabulary
+ *   position [n_position x d]    recency rank p_j = (last row of the request) - j, clamped to n_position - 1
+ *   tdelta   [n_tdelta x d] or NULL: bucket floor(log2(req_time[b] - timestamp[j])) for a delta >= 1 s,
+ *                                    0 otherwise, clamped to n_tdelta - 1
+ * (readings R-N4a-c; the paper fixes none of the three). */
+typedef struct {
+  const void *video;
+  int64_t n_video;
+  const void *action;
+  int64_t n_action;
+  const void *position;
+  int64_t n_position;
+  const void *tdelta;
+  int64_t n_tdelta;
+} stca_embed_tables;
+
+/* X [T x d] (storage dtype) for the ragged batch hist_off [B+1] (device int64): x_j = video[v'_j] +
+ * action[a'_j] + position[p_j] (+ tdelta[bucket_j]) summed in fp32 in that order, rounded once.
+ * video_id / action_id / timestamp int64 [T], req_time int64 [B] (timestamp / req_time may be NULL
+ * without a tdelta table).  The result feeds stca_project_history directly.  Asynchronous on
+ * `stream`.  INVALID_ARG for NULL / negative / misaligned arguments, UNSUPPORTED if d * element size
+ * is not a multiple of 16 bytes. */
+stca_status stca_encode_history(const stca_embed_tables *tables, int32_t d, int32_t dtype, const int64_t *video_id,
+                                const int64_t *action_id, const int64_t *timestamp, const int64_t *hist_off,
+                                const int64_t *req_time, int64_t B, int64_t T, void *X, void *stream);
 
 #ifdef __cplusplus
 }

@@ -20,11 +20,11 @@ import numpy as np
 
 from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_persistent, plan_shards,  # noqa: F401,E501
                    plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, ALLOC_FN,
-                   FREE_FN, PHASES, _Config, _Tensor, LIB_PATH)
+                   FREE_FN, PHASES, _Config, _Tensor, _EmbedTables, LIB_PATH)
 
 __all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_persistent", "plan_shards", "plan_split", "plan_suffix",
            "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange", "rlb_allocate",
-           "rlb_compact"]
+           "rlb_compact", "encode_history"]
 
 
 def _ptr(x) -> int:
@@ -165,8 +165,12 @@ class STCA:
         self._check(lib().stca_debug_capture(self._h, int(layer), ctypes.c_void_p(_ptr(U)), ctypes.c_void_p(_ptr(Y))))
 
     # -- per-phase device timing (stca_profile) --
-    def profile(self, enable: bool = True) -> None:
-        self._check(lib().stca_profile(self._h, 1 if enable else 0))
+    PROF_EVENTS, PROF_TWICE_ATTENTION, PROF_TWICE_PROJECT = 1, 2, 4
+
+    def profile(self, enable=True) -> None:
+        """True / False: per-phase event regions; an int: the STCA_PROF_* bit mask (include/stca.h)."""
+        mask = int(enable) if not isinstance(enable, bool) else (1 if enable else 0)
+        self._check(lib().stca_profile(self._h, mask))
 
     def profile_read(self):
         """{phase: (total ms, regions)} since the last read (waits for the recorded events)."""
@@ -185,6 +189,27 @@ class STCA:
                                                 off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
                                                 ctypes.c_void_p(_stream(stream))))
         self._B = B
+
+    def session_open(self, capacity_rows: int, stream=None) -> None:
+        """Persistent per-user X~ cache (NEXT-4); see stca_session_open."""
+        self._check(lib().stca_session_open(self._h, int(capacity_rows), ctypes.c_void_p(_stream(stream))))
+
+    def project_history_session(self, user_id, gen, X, hist_off, stream=None) -> int:
+        """stca_project_history_session: projects only users not cached with the same generation; returns the
+        number of users projected."""
+        off = _i64(hist_off)
+        B = off.shape[0] - 1
+        u, g = _i64(user_id), _i64(gen)
+        if u.shape[0] != B or g.shape[0] != B:
+            raise ValueError("user_id / gen need one entry per request")
+        n = ctypes.c_int64(0)
+        p64 = ctypes.POINTER(ctypes.c_int64)
+        self._check(lib().stca_project_history_session(self._h, u.ctypes.data_as(p64), g.ctypes.data_as(p64),
+                                                        ctypes.c_void_p(_ptr(X)), int(X.shape[0]),
+                                                        off.ctypes.data_as(p64), B, ctypes.byref(n),
+                                                        ctypes.c_void_p(_stream(stream))))
+        self._B = B
+        return int(n.value)
 
     def read_cache(self, layer: int, row0: int = 0, nrows: Optional[int] = None, out=None, stream=None):
         """Rows of the projected X~(layer) cache (compacted order) as float32; returns `out` (a new host
@@ -315,3 +340,27 @@ def rlb_compact(X, hist_off, alloc, new_off, L_avg: int, P=None, stream=None):
     if st != 0:
         raise StcaError(st, "stca_rlb_compact")
     return P, seg_off, segs
+
+
+def encode_history(video, action, position, video_id, action_id, hist_off, tdelta=None, timestamp=None,
+                   req_time=None, X=None, stream=None):
+    """stca_encode_history (include/stca.h): X [T x d] from ids.  Tables: CUDA tensors
+    (bf16 as int16 bit patterns, or float32), video [V+1 x d] / action [A+1 x d] with the OOV row last,
+    position [P x d], tdelta [NB x d] or None; ids / timestamps int64 [T], hist_off int64 [B+1],
+    req_time int64 [B] (CUDA).  Returns X (same dtype as the tables)."""
+    import torch
+    d = int(video.shape[1])
+    bf16 = video.dtype in (torch.int16, torch.bfloat16)
+    T = int(video_id.shape[0])
+    B = int(hist_off.shape[0]) - 1
+    if X is None:
+        X = torch.empty((T, d), dtype=video.dtype, device=video.device)
+    tab = _EmbedTables(_ptr(video), int(video.shape[0]) - 1, _ptr(action), int(action.shape[0]) - 1,
+                       _ptr(position), int(position.shape[0]), _ptr(tdelta) if tdelta is not None else None,
+                       int(tdelta.shape[0]) if tdelta is not None else 0)
+    st = lib().stca_encode_history(ctypes.byref(tab), d, STCA_BF16 if bf16 else STCA_FP32, _ptr(video_id),
+                                   _ptr(action_id), _ptr(timestamp), _ptr(hist_off), _ptr(req_time), B, T,
+                                   _ptr(X), _stream(stream))
+    if st != 0:
+        raise StcaError(st, "stca_encode_history")
+    return X

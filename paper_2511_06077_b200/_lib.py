@@ -32,6 +32,12 @@ class _Tensor(ctypes.Structure):
                 ("cols", ctypes.c_int64)]
 
 
+class _EmbedTables(ctypes.Structure):
+    _fields_ = [("video", ctypes.c_void_p), ("n_video", ctypes.c_int64), ("action", ctypes.c_void_p),
+                ("n_action", ctypes.c_int64), ("position", ctypes.c_void_p), ("n_position", ctypes.c_int64),
+                ("tdelta", ctypes.c_void_p), ("n_tdelta", ctypes.c_int64)]
+
+
 class StcaError(RuntimeError):
     def __init__(self, status: int, message: str = ""):
         super().__init__(f"{status_string(status)} ({status}): {message}")
@@ -45,7 +51,8 @@ SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy"
            "stca_status_string", "stca_abi_version", "stca_validate_offsets", "stca_plan_suffix",
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
            "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact",
-           "stca_profile", "stca_profile_read"]
+           "stca_profile", "stca_profile_read", "stca_session_open", "stca_project_history_session",
+           "stca_encode_history"]
 
 
 def lib():
@@ -102,6 +109,16 @@ def lib():
         L.stca_read_cache.restype = ctypes.c_int
         L.stca_debug_capture.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
         L.stca_debug_capture.restype = ctypes.c_int32
+        L.stca_encode_history.argtypes = [ctypes.POINTER(_EmbedTables), ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                          ctypes.c_void_p]
+        L.stca_encode_history.restype = ctypes.c_int32
+        L.stca_session_open.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.stca_session_open.restype = ctypes.c_int32
+        L.stca_project_history_session.argtypes = [ctypes.c_void_p, _I64P, _I64P, ctypes.c_void_p, ctypes.c_int64,
+                                                   _I64P, ctypes.c_int64, _I64P, ctypes.c_void_p]
+        L.stca_project_history_session.restype = ctypes.c_int32
         L.stca_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.stca_profile.restype = ctypes.c_int32
         L.stca_profile_read.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _I64P]

@@ -21,7 +21,8 @@ OUT = os.path.join(PKG, "libstca.so")
 BUILD = os.path.join(ROOT, "build", "stca")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "kernels_cc.cu", "tc_gemm.cu", "tc_host.cu", "tc_proj.cu", "tc_attn.cu", "tc_attn_wide.cu", "tc_attn_narrow.cu", "rlb_batch.cu"]
+SOURCES = ["api.cu", "kernels_cc.cu", "tc_gemm.cu", "tc_host.cu", "tc_proj.cu", "tc_attn.cu", "tc_attn_wide.cu", "tc_attn_narrow.cu", "rlb_batch.cu",
+           "encode.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
@@ -34,11 +35,11 @@ def _deps_mtime() -> float:
     return m
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, src + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, verbose: bool, defines=(), build_dir: str = BUILD) -> str:
+    obj = os.path.join(build_dir, src + ".o")
+    cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(BUILD, src + ".log")
+    log = os.path.join(build_dir, src + ".log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
     if p.returncode != 0:
@@ -49,21 +50,27 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str = "") -> str:
+    """variant/defines: an A/B build (e.g. -DSTCA_NARROW_PF=0) as libstca_<variant>.so, loaded with
+    STCA_LIB=<path>; never used by the product's default import."""
+    out = OUT if not variant else os.path.join(PKG, f"libstca_{variant}.so")
+    bdir = BUILD if not variant else os.path.join(ROOT, "build", "stca_" + variant)
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= _deps_mtime():
+        return out
+    os.makedirs(bdir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    tmp = OUT + ".tmp"
+        objs = list(ex.map(lambda s: _compile(s, verbose, defines, bdir), SOURCES))
+    tmp = out + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.defines, a.variant))

@@ -154,26 +154,36 @@ struct stca_handle {
   int64_t T2 = 0;
   Alloc al;
   DevBuf xt_cache;  // M x [T2 x d] storage
-  DevBuf xin, xgather, seg, proj_h, proj_y;
+  DevBuf xin[2], xgather, seg, proj_h, proj_y;  // xin: double-buffered host-input staging
   // forward scratch
   DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, ctal, zout, Zout;
   StagingRing stage;
+  // session cache (stca_session_open / stca_project_history_session): X~ rows per user across calls
+  struct SessEntry {
+    int64_t gen, len, off;
+  };
+  bool sess_on = false;
+  int64_t sess_cap = 0, sess_head = 0;
+  std::map<int64_t, SessEntry> sess;      // user -> entry
+  std::map<int64_t, int64_t> sess_pos;    // cache row offset -> user (ordered, for eviction by overlap)
   // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
   int cap_layer = 0;
   void *cap_U = nullptr, *cap_Y = nullptr;
   // stca_profile
   bool prof = false;
+  int reps_attn = 1, reps_proj = 1;  // STCA_PROF_TWICE_*
   std::vector<ProfRegion> prof_open;  // recorded, not yet read
   std::vector<cudaEvent_t> prof_pool;
   int64_t chunk_cap = STCA_DEFAULT_CHUNK_KEYS;
   // pipelined host-input projection: copy stream + one event per piece
   cudaStream_t copy_st = nullptr;
-  cudaEvent_t ev_xin_free = nullptr, ev[STCA_H2D_PIECES] = {};
+  cudaEvent_t ev_xin_free[2] = {}, ev[STCA_H2D_PIECES] = {};
+  int xin_k = 0;  // staging buffer of the next host-input projection
 };
 
 static DevBuf *const *all_bufs(stca_handle *h, int *n) {
   static thread_local DevBuf *v[32];
-  DevBuf *list[] = {&h->xt_cache, &h->xin,  &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
+  DevBuf *list[] = {&h->xt_cache, &h->xin[0], &h->xin[1], &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
                     &h->part,     &h->partg, &h->items,  &h->mitems, &h->ctal,   &h->zout,   &h->Zout};
   *n = (int)(sizeof list / sizeof list[0]);
@@ -668,7 +678,7 @@ extern "C" void stca_destroy(stca_handle *h) {
   for (cudaEvent_t e : h->prof_pool) cudaEventDestroy(e);
   if (h->copy_st) {
     cudaStreamDestroy(h->copy_st);
-    cudaEventDestroy(h->ev_xin_free);
+    for (cudaEvent_t e : h->ev_xin_free) cudaEventDestroy(e);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   }
   cudaGetLastError();
@@ -726,7 +736,7 @@ static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64
       pj.H = h->proj_h.p;
     }
     cudaEvent_t pa = prof_begin(h, st);
-    CU(stca::tc_project(pj, st));
+    for (int rep = 0; rep < h->reps_proj; ++rep) CU(stca::tc_project(pj, st));  // idempotent
     prof_end(h, STCA_PH_PROJECT, pa, st);
     return STCA_OK;
   }
@@ -749,9 +759,9 @@ static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64
   return STCA_OK;
 }
 
-extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
-                                            int64_t B, void *stream) {
-  if (!h) return STCA_ERR_INVALID_ARG;
+// validation of a projection call (nothing is enqueued on failure): offsets, empty histories, the
+// split-K fold's chunk limit
+static stca_status validate_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off, int64_t B) {
   if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
   if (B < 0 || T < 0 || !hist_off || (T > 0 && !X)) return fail(h, STCA_ERR_INVALID_ARG, "NULL or negative argument");
   int64_t badi = -1;
@@ -767,6 +777,17 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
       return fail(h, STCA_ERR_UNSUPPORTED, "history %lld has %lld keys > 8 x chunk_keys (%lld); raise chunk_keys",
                   (long long)b, (long long)Lb, (long long)h->chunk_cap);
   }
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64_t T, const int64_t *hist_off,
+                                            int64_t B, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  stca_status s = validate_history(h, X, T, hist_off, B);
+  if (s != STCA_OK) return s;
+  h->sess_on = false;  // a plain projection replaces any session cache (its entries are forgotten)
+  h->sess.clear();
+  h->sess_pos.clear();
   CU(cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
   const int d = h->cfg.d, M = h->cfg.M, es = h->es;
@@ -800,22 +821,28 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     // it has landed, so the H2D copy (the e2e bottleneck) overlaps the projection of earlier pieces
     if (!h->copy_st) {
       CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
-      CU(cudaEventCreateWithFlags(&h->ev_xin_free, cudaEventDisableTiming));
+      for (cudaEvent_t &e : h->ev_xin_free) {  // recorded now: uploads wait for every earlier reader on `stream`
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CU(cudaEventRecord(e, st));
+      }
       for (cudaEvent_t &e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    void *const xin_old = h->xin.p;
-    CU(h->xin.ensure((size_t)T * row_bytes, st));
-    // a regrown xin was allocated in `stream` order: the copy stream may write it only after that point
-    if (h->xin.p != xin_old) CU(cudaEventRecord(h->ev_xin_free, st));
-    // the copies only wait for the previous projection's reads of xin (ev_xin_free), not for other
-    // work on `stream`: the next request batch's upload overlaps the current forward
-    CU(cudaStreamWaitEvent(h->copy_st, h->ev_xin_free, 0));
+    // two staging buffers in turn: the upload of call n + 1 waits only for the projection of call n - 1
+    // (its buffer's last reader), so the PCIe copies of consecutive calls run back to back
+    const int xk = h->xin_k;
+    h->xin_k ^= 1;
+    DevBuf &xin = h->xin[xk];
+    void *const xin_old = xin.p;
+    CU(xin.ensure((size_t)T * row_bytes, st));
+    // a regrown buffer was allocated in `stream` order: the copy stream may write it only after that point
+    if (xin.p != xin_old) CU(cudaEventRecord(h->ev_xin_free[xk], st));
+    CU(cudaStreamWaitEvent(h->copy_st, h->ev_xin_free[xk], 0));
     const int npieces = (int)std::min<int64_t>(STCA_H2D_PIECES, (T2 + (1 << 16) - 1) >> 16);
     const int64_t step = ((T2 + npieces - 1) / npieces + 255) / 256 * 256;  // whole 128-row tile pairs
     int k = 0;
     for (int64_t r0 = 0; r0 < T2; r0 += step, ++k) {
       const int64_t rows = std::min<int64_t>(step, T2 - r0);
-      uint8_t *dst = (uint8_t *)h->xin.p + (size_t)r0 * row_bytes;
+      uint8_t *dst = (uint8_t *)xin.p + (size_t)r0 * row_bytes;
       CU(cudaMemcpyAsync(dst, (const uint8_t *)X + (size_t)r0 * row_bytes, (size_t)rows * row_bytes,
                          cudaMemcpyHostToDevice, h->copy_st));
       CU(cudaEventRecord(h->ev[k], h->copy_st));
@@ -823,14 +850,16 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
       stca_status s = project_rows(h, dst, r0, rows, st);
       if (s != STCA_OK) return s;
     }
-    CU(cudaEventRecord(h->ev_xin_free, st));
+    CU(cudaEventRecord(h->ev_xin_free[xk], st));
     h->B = B;
     return STCA_OK;
   }
   if (host_x) {  // host input with a gather: stage all of X on the stream first
-    CU(h->xin.ensure((size_t)T * row_bytes, st));
-    CU(cudaMemcpyAsync(h->xin.p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
-    Xd = h->xin.p;
+    // on `stream` itself (ordered after every earlier reader); the copy stream's next upload into this
+    // buffer is ordered after this call's projection by ev_xin_free below
+    CU(h->xin[0].ensure((size_t)T * row_bytes, st));
+    CU(cudaMemcpyAsync(h->xin[0].p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
+    Xd = h->xin[0].p;
   }
   if (gather && T2 > 0) {  // gather the (owned) suffix rows into a compacted buffer
     std::vector<int64_t> seg;
@@ -857,7 +886,159 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
     stca_status s = project_rows(h, Xd, 0, T2, st);
     if (s != STCA_OK) return s;
   }
-  if (host_x && h->ev_xin_free) CU(cudaEventRecord(h->ev_xin_free, st));
+  if (host_x && h->ev_xin_free[0]) CU(cudaEventRecord(h->ev_xin_free[0], st));
+  h->B = B;
+  return STCA_OK;
+}
+
+// ===========================================================================
+// session sharing (NEXT-4): RLB extended across requests of the same user
+// ===========================================================================
+extern "C" stca_status stca_session_open(stca_handle *h, int64_t capacity_rows, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (capacity_rows < 1) return fail(h, STCA_ERR_INVALID_ARG, "capacity_rows must be >= 1");
+  if (h->cfg.split_world > 1) return fail(h, STCA_ERR_UNSUPPORTED, "no session cache in split-history mode");
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  h->B = -1;
+  CU(h->xt_cache.ensure((size_t)h->cfg.M * capacity_rows * h->cfg.d * h->es + 256, st));
+  h->sess_on = true;
+  h->sess_cap = capacity_rows;
+  h->sess_head = 0;
+  h->sess.clear();
+  h->sess_pos.clear();
+  h->T2 = capacity_rows;  // rows per layer of the cache
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_project_history_session(stca_handle *h, const int64_t *user_id, const int64_t *gen,
+                                                    const void *X, int64_t T, const int64_t *hist_off, int64_t B,
+                                                    int64_t *n_projected, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (!h->sess_on) return fail(h, STCA_ERR_STATE, "stca_project_history_session before stca_session_open");
+  if (B > 0 && (!user_id || !gen)) return fail(h, STCA_ERR_INVALID_ARG, "user_id / gen is NULL");
+  stca_status s = validate_history(h, X, T, hist_off, B);
+  if (s != STCA_OK) return s;
+  // a0: the temporal suffix of every request
+  std::vector<int64_t> start(B), len(B);
+  stca_plan_suffix(hist_off, B, h->cfg.L_infer, start.data());
+  int64_t total = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    len[b] = hist_off[b + 1] - start[b];
+    total += len[b];
+  }
+  // Hits: (user, generation, kept length) in the cache; a user twice in one batch with the same key
+  // shares one entry.  The misses get ONE contiguous range of the FIFO ring (one projection launch);
+  // entries it overlaps are evicted.  If that would evict a hit of this batch, the cache is reset and
+  // the whole batch projected from row 0.
+  std::vector<int64_t> miss;  // first request of every missing user, in request order
+  int64_t a = 0, R = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      h->sess.clear();
+      h->sess_pos.clear();
+      h->sess_head = 0;
+    }
+    miss.clear();
+    R = 0;
+    std::map<int64_t, int64_t> hit_users, miss_users;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t u = user_id[b];
+      auto it = h->sess.find(u);
+      const bool cached = it != h->sess.end() && it->second.gen == gen[b] && it->second.len == len[b];
+      auto mu = miss_users.find(u);
+      if (mu != miss_users.end()) {  // already missing in this batch: must be the same (gen, length)
+        if (gen[mu->second] != gen[b] || len[mu->second] != len[b])
+          return fail(h, STCA_ERR_INVALID_ARG, "user %lld appears twice in the batch with different histories",
+                      (long long)u);
+      } else if (cached) {
+        hit_users[u] = b;
+      } else {
+        miss_users[u] = b;
+        miss.push_back(b);
+        R += len[b];
+      }
+    }
+    for (auto &hu : hit_users)
+      if (miss_users.count(hu.first)) return fail(h, STCA_ERR_INVALID_ARG, "user %lld appears twice in the batch "
+                                                  "with different histories", (long long)hu.first);
+    if (R > h->sess_cap)
+      return fail(h, STCA_ERR_OOM, "the batch needs %lld new cache rows, capacity %lld", (long long)R,
+                  (long long)h->sess_cap);
+    a = h->sess_head + R <= h->sess_cap ? h->sess_head : 0;
+    std::vector<int64_t> evict;
+    bool hit_evicted = false;
+    for (auto &p : h->sess_pos) {
+      const auto &e = h->sess[p.second];
+      if (R > 0 && e.off < a + R && e.off + e.len > a) {
+        evict.push_back(p.second);
+        hit_evicted |= hit_users.count(p.second) > 0;
+      }
+    }
+    if (hit_evicted && attempt == 0) continue;  // reset and project the whole batch
+    for (int64_t u : evict) {
+      h->sess_pos.erase(h->sess[u].off);
+      h->sess.erase(u);
+    }
+    int64_t off = a;
+    for (int64_t b : miss) {  // (re)place every missing user's entry
+      auto it = h->sess.find(user_id[b]);
+      if (it != h->sess.end()) {
+        h->sess_pos.erase(it->second.off);
+        h->sess.erase(it);
+      }
+      h->sess[user_id[b]] = {gen[b], len[b], off};
+      h->sess_pos[off] = user_id[b];
+      off += len[b];
+    }
+    h->sess_head = a + R;
+    break;
+  }
+  (void)total;
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t row_bytes = (size_t)h->cfg.d * h->es;
+  h->B = -1;
+  h->start = start;
+  h->len = len;
+  h->olen = len;
+  h->own0.assign(B, 0);
+  h->coff.assign(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b) h->coff[b] = h->sess[user_id[b]].off;  // key rows of request b in the cache
+  h->coff[B] = h->sess_cap;
+  h->T2 = h->sess_cap;
+  if (R > 0) {  // gather the missing users' suffix rows, project them into cache rows [a, a + R)
+    const void *Xd = X;
+    if (!is_device_ptr(X)) {
+      CU(h->xin[0].ensure((size_t)T * row_bytes, st));
+      CU(cudaMemcpyAsync(h->xin[0].p, X, (size_t)T * row_bytes, cudaMemcpyHostToDevice, st));
+      Xd = h->xin[0].p;
+    }
+    std::vector<int64_t> seg;
+    int64_t maxlen = 0, dst = 0;
+    for (int64_t b : miss) {
+      seg.push_back(start[b]);
+      seg.push_back(dst);
+      seg.push_back(len[b]);
+      dst += len[b];
+      maxlen = std::max(maxlen, len[b]);
+    }
+    CU(h->seg.ensure(seg.size() * 8, st));
+    void *slot = nullptr;
+    cudaEvent_t slot_ev = nullptr;
+    s = staging_acquire(h, seg.size() * 8, &slot, &slot_ev);
+    if (s != STCA_OK) return s;
+    memcpy(slot, seg.data(), seg.size() * 8);
+    CU(cudaMemcpyAsync(h->seg.p, slot, seg.size() * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(slot_ev, st));
+    CU(h->xgather.ensure((size_t)R * row_bytes, st));
+    CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), (int64_t)miss.size(), maxlen, (int)row_bytes, st));
+    s = project_rows(h, h->xgather.p, a, R, st);
+    if (s != STCA_OK) return s;
+    if (h->ev_xin_free[0]) CU(cudaEventRecord(h->ev_xin_free[0], st));
+  }
+  if (n_projected) *n_projected = (int64_t)miss.size();
   h->B = B;
   return STCA_OK;
 }
@@ -1111,6 +1292,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     if (s != STCA_OK) return s;
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     cudaEvent_t pa = prof_begin(h, st);
+    for (int rep = 0; rep < h->reps_attn; ++rep) {  // idempotent (STCA_PROF_TWICE_ATTENTION)
     if (tc_attn) {
       if (nit_nar > 0)
         CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg,
@@ -1124,6 +1306,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
                                  h->part.as<float>(), st));
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+    }
     }
     prof_end(h, STCA_PH_ATTENTION, pa, st);
     const float *merged_from = h->part.as<float>();
@@ -1176,7 +1359,9 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
 // ===========================================================================
 extern "C" stca_status stca_profile(stca_handle *h, int32_t enable) {
   if (!h) return STCA_ERR_INVALID_ARG;
-  h->prof = enable != 0;
+  h->prof = (enable & STCA_PROF_EVENTS) != 0;
+  h->reps_attn = (enable & STCA_PROF_TWICE_ATTENTION) ? 2 : 1;
+  h->reps_proj = (enable & STCA_PROF_TWICE_PROJECT) ? 2 : 1;
   return STCA_OK;
 }
 

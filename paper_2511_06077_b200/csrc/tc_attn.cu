@@ -59,6 +59,9 @@ constexpr int AT_STAGE_BYTES = AT_BM * AT_YSTRIDE;  // 34 KB epilogue staging; t
 constexpr int AT_MAXI = 128;                  // work items of a CTA cached in shared memory
 constexpr int AT_SMEM = 1024 + AT_STAGES * AT_X_BYTES + AT_STAGE_BYTES + AT_MAXI * (int)sizeof(AttnItem) + 256;
 constexpr float AT_RESCALE_THRESHOLD = 8.f;    // log2(256)
+#ifndef STCA_ATTN_PF
+#define STCA_ATTN_PF 4  // key tiles prefetched into L2 ahead of the TMA loads (0: off)
+#endif
 constexpr int AT_WP = AT_NSW, AT_WS = AT_NSW + 1, AT_WO = AT_NSW + 2, AT_THREADS = 32 * (AT_NSW + 3);
 constexpr uint32_t AT_TS = 0, AT_TO = 256, AT_TU = 384;  // TMEM columns: S0 | S1 | O | U0 | U1
 
@@ -124,6 +127,29 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     if (lane == 0) {  // ---------------- TMA producer: U tiles and the X~ ring ----------------
       const uint64_t pol_x = policy_evict_first();
       int s = 0, ph = 0;
+      // L2 prefetch cursor, STCA_ATTN_PF key tiles ahead of the loads, across item boundaries
+      int pf_k = 0, pf_j = 0, pf_nt = 0;
+      int64_t pf_key0 = 0;
+      if (ni > 0) {
+        const AttnItem f = item(0);
+        pf_nt = (f.klen + AT_BN - 1) / AT_BN;
+        pf_key0 = f.key0;
+      }
+      auto pf_step = [&]() {
+        if (pf_k >= ni) return;
+        const int32_t row = (int32_t)(pf_key0 + (int64_t)pf_j * AT_BN);
+        tma_prefetch_l2(&mapX, 0, row);
+        tma_prefetch_l2(&mapX, 64, row);
+        if (++pf_j >= pf_nt) {
+          pf_j = 0;
+          if (++pf_k < ni) {
+            const AttnItem f = item(pf_k);
+            pf_nt = (f.klen + AT_BN - 1) / AT_BN;
+            pf_key0 = f.key0;
+          }
+        }
+      };
+      for (int k = 0; k < STCA_ATTN_PF; ++k) pf_step();
       for (int k = 0; k < ni; ++k) {
         const AttnItem it = item(k);
         // U of item k into the staging area once the softmax warps moved U(k-1) into TMEM and the
@@ -134,6 +160,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tma_load_2d(sStage + AT_U_BYTES / 2, &mapU, us_full, 64, (int32_t)it.qrow0);
         const int nt = (it.klen + AT_BN - 1) / AT_BN;
         for (int j = 0; j < nt; ++j) {
+          if (STCA_ATTN_PF > 0) pf_step();
           mbar_wait(&x_empty[s], ph ^ 1);
           uint8_t *dst = sX + s * AT_X_BYTES;
           const int32_t row = (int32_t)(it.key0 + (int64_t)j * AT_BN);

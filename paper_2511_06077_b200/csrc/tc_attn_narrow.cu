@@ -29,6 +29,9 @@
 #ifndef STCA_NARROW_LAZY
 #define STCA_NARROW_LAZY 8.f  // rescale threshold in log2 units (a test build sets 0)
 #endif
+#ifndef STCA_NARROW_PF
+#define STCA_NARROW_PF 6  // key tiles prefetched into L2 ahead of the TMA loads (0: off)
+#endif
 
 namespace stca {
 namespace tc {
@@ -38,7 +41,10 @@ bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, 
 struct NCfg {
   static constexpr int D = 128, BK = 128, NQ = 64;    // d, keys per tile, query columns
   static constexpr int X_BYTES = BK * D * 2;           // 2 boxes of 128 keys x 64 d (16 KB each)
-  static constexpr int STAGES = 4;
+  // 5 stages: a tile holds its slot from the TMA issue until its PV completes (~2 slots busy with
+  // S / softmax / PV), so the slots left in flight bound the HBM bytes in flight per SM; the L2
+  // prefetch (STCA_NARROW_PF tiles ahead) takes the HBM latency off the ring.  SMEM: 226.3 of 227 KB.
+  static constexpr int STAGES = 5;
   static constexpr int P_BYTES = BK * NQ * 2;          // P^T: 128 keys x 64 queries, SW128 (16 KB)
   static constexpr int U_BYTES = NQ * D * 2;           // U: 64 queries x 128 d, 2 boxes of 8 KB
   static constexpr int RED_BYTES = 4 * 4 * 16 * 4;     // [column group][quarter][16] column partials
@@ -128,6 +134,29 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
   if (warp == C::NSW) {
     if (lane == 0) {  // ---------------- TMA producer: per item U, then its key tiles ----------------
       int s = 0, ph = 0;
+      // L2 prefetch cursor, STCA_NARROW_PF key tiles ahead of the loads, across item boundaries
+      int pf_n = i0, pf_j = 0, pf_nt = 0;
+      int64_t pf_key0 = 0;
+      if (i0 < i1) {
+        const AttnItem f = items[cta_items[i0]];
+        pf_nt = (f.klen + C::BK - 1) / C::BK;
+        pf_key0 = f.key0;
+      }
+      auto pf_step = [&]() {  // prefetch the tile under the cursor, then advance it
+        if (pf_n >= i1) return;
+        const int32_t row = (int32_t)(pf_key0 + (int64_t)pf_j * C::BK);
+        tma_prefetch_l2(&mapX, 0, row);
+        tma_prefetch_l2(&mapX, 64, row);
+        if (++pf_j >= pf_nt) {
+          pf_j = 0;
+          if (++pf_n < i1) {
+            const AttnItem f = items[cta_items[pf_n]];
+            pf_nt = (f.klen + C::BK - 1) / C::BK;
+            pf_key0 = f.key0;
+          }
+        }
+      };
+      for (int k = 0; k < STCA_NARROW_PF; ++k) pf_step();
       for (int n = i0; n < i1; ++n) {
         const AttnItem it = items[cta_items[n]];
         const int ni = n - i0, ub = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
@@ -137,6 +166,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         tma_load_2d(ud, &mapU, &u_full[ub], 0, (int32_t)it.qrow0);  // rows past nq: finite, unused columns
         tma_load_2d(ud + C::U_BYTES / 2, &mapU, &u_full[ub], 64, (int32_t)it.qrow0);
         for (int j = 0; j < nt; ++j) {
+          if (STCA_NARROW_PF > 0) pf_step();
           mbar_wait(&x_empty[s], ph ^ 1);
           uint8_t *dst = sX + s * C::X_BYTES;
           const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BK);

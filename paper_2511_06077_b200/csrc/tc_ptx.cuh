@@ -66,6 +66,11 @@ __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *m
       "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// 2-D tile prefetch into L2 (no shared memory, no barrier): a later tma_load of the same box hits L2,
+// so the bytes in flight from HBM are not bounded by the shared-memory ring
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(m), "r"(c0), "r"(c1) : "memory");
+}
 // multicast 2-D tile load: same smem offset + mbarrier offset in every CTA of ctaMask (cluster)
 __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
                                                uint16_t mask, uint64_t policy) {
