@@ -314,33 +314,11 @@ def main():
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / K
 
-    def timed_loop(mask):
-        """K steps with the library issuing the attention (or projection) launches twice (identical
-        results): the step-time difference is their marginal duration in the real pipeline."""
-        model.profile(mask)
-        step()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        for _ in range(K):
-            step()
-        b.record(st)
-        torch.cuda.synchronize()
-        model.profile(0)
-        return a.elapsed_time(b) / K
-
-    marg = None
-    if not args.no_profile:
-        ms_attn2 = timed_loop(stca.STCA.PROF_TWICE_ATTENTION)
-        ms_proj2 = timed_loop(stca.STCA.PROF_TWICE_PROJECT)
-        marg = {"attention_ms_per_launch": (ms_attn2 - ms) / c.M, "project_ms_per_launch": ms_proj2 - ms,
-                "step_ms_attention_twice": ms_attn2, "step_ms_project_twice": ms_proj2}
-
     # profiled pass (separate from the timed one): per-phase CUDA events on the launching stream
     prof = None
     if not args.no_profile:
         model.profile(True)
-        Kp = max(1, min(K, 5))
+        Kp = max(1, min(K, 10))
         for _ in range(Kp):
             step()
         prof = {k: (v[0] / Kp, v[1] // Kp) for k, v in model.profile_read().items()}  # per step: (ms, regions)
@@ -394,15 +372,19 @@ def main():
         peak_kind = "sustained" if ("sw_power_cap" in reasons or timed_s > 1.0) else "burst"
         alg = algorithmic(wl)  # rank 0's shard
         kernels = []
-        if marg:  # marginal launch durations (CUDA events over whole timed regions; see timed_loop)
-            kernels.append(roofline_entry("history projection (a1, k_tc_project)", "project", alg["proj_flops"],
-                                          alg["proj_bytes"], marg["project_ms_per_launch"], pk, peak_kind, c.name))
-            kernels.append(roofline_entry("ragged single-query attention (a4, one layer)", "attention",
-                                          alg["attn_flops_layer"], alg["attn_bytes_layer"],
-                                          marg["attention_ms_per_launch"], pk, peak_kind, c.name))
+        if prof:  # CUDA-event regions on the launching stream around each projection / attention launch
+            if prof["project"][1]:
+                kernels.append(roofline_entry("history projection (a1, k_tc_project)", "project", alg["proj_flops"],
+                                              alg["proj_bytes"], prof["project"][0] / prof["project"][1], pk,
+                                              peak_kind, c.name))
+            if prof["attention"][1]:
+                kernels.append(roofline_entry("ragged single-query attention (a4, one layer)", "attention",
+                                              alg["attn_flops_layer"], alg["attn_bytes_layer"],
+                                              prof["attention"][0] / prof["attention"][1], pk, peak_kind, c.name))
             for k in kernels:
-                k["timing"] = ("marginal: (step time with this launch issued twice - step time) over K timed steps, "
-                               "CUDA events on the launching stream")
+                k["timing"] = ("CUDA events on the launching stream around the launch, K steps after the timed "
+                               "region (an upper bound of the kernel time: the events also hold its launch and "
+                               "take away the programmatic-dependent-launch overlap)")
         step_ms_prof = (prof["project"][0] + prof["forward"][0]) if prof else None
         dom = None
         if kernels:  # the dominant kernel by time share of the step
@@ -416,11 +398,10 @@ def main():
             phases = {"project_ms": prof["project"][0], "forward_ms": prof["forward"][0],
                       "attention_ms_per_layer": prof["attention"][0] / max(prof["attention"][1], 1),
                       "merge_ms_per_layer": prof["merge"][0] / max(prof["merge"][1], 1) if prof["merge"][1] else 0.0,
-                      "target_side_ms": prof["target"][0], "target_side_launches": prof["target"][1],
                       "targets_per_s_cached_history": wl.Nt / (prof["forward"][0] * 1e-3),
                       "source": "stca_profile events on the launching stream (separate pass; an upper bound of "
                                 "the unprofiled step: events break programmatic-dependent-launch overlap)",
-                      "step_ms_profiled": step_ms_prof, "marginal": marg}
+                      "step_ms_profiled": step_ms_prof}
         loads = [r[0] for r in per_rank]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,

@@ -177,13 +177,14 @@ stca_status stca_read_cache(stca_handle *h, int32_t layer, int64_t row0, int64_t
  * dependent-launch overlap across them, so profiled phase times are upper bounds of unprofiled
  * ones.  stca_profile_read waits for the recorded events, writes the total milliseconds and the
  * region count of every phase since the last read (arrays of STCA_PH_N) and resets.
- * `enable` is a bit mask: STCA_PROF_EVENTS (the regions above), STCA_PROF_TWICE_ATTENTION (every a4
- * launch is issued twice: identical results, so the step-time difference over a timed region is
- * the attention launches' marginal duration inside the real, PDL-overlapped pipeline) and
- * STCA_PROF_TWICE_PROJECT (the same for the a1 projection launch). */
+ * `enable` is a bit mask: STCA_PROF_EVENTS (the project / attention / merge / forward regions),
+ * STCA_PROF_EVENTS_TARGET (also a region around every target-side GEMM launch: more perturbation),
+ * STCA_PROF_TWICE_ATTENTION / STCA_PROF_TWICE_PROJECT (every a4 / a1 launch is issued twice with
+ * identical results -- a diagnostic: the step-time difference is the launches' marginal cost, which
+ * power management inflates, so the bench does not use it as a kernel duration). */
 enum { STCA_PH_PROJECT = 0, STCA_PH_ATTENTION = 1, STCA_PH_MERGE = 2, STCA_PH_TARGET = 3, STCA_PH_FORWARD = 4,
        STCA_PH_N = 5 };
-enum { STCA_PROF_EVENTS = 1, STCA_PROF_TWICE_ATTENTION = 2, STCA_PROF_TWICE_PROJECT = 4 };
+enum { STCA_PROF_EVENTS = 1, STCA_PROF_TWICE_ATTENTION = 2, STCA_PROF_TWICE_PROJECT = 4, STCA_PROF_EVENTS_TARGET = 8 };
 stca_status stca_profile(stca_handle *h, int32_t enable);
 stca_status stca_profile_read(stca_handle *h, double *ms, int64_t *count);
 

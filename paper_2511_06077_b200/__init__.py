@@ -165,7 +165,7 @@ class STCA:
         self._check(lib().stca_debug_capture(self._h, int(layer), ctypes.c_void_p(_ptr(U)), ctypes.c_void_p(_ptr(Y))))
 
     # -- per-phase device timing (stca_profile) --
-    PROF_EVENTS, PROF_TWICE_ATTENTION, PROF_TWICE_PROJECT = 1, 2, 4
+    PROF_EVENTS, PROF_TWICE_ATTENTION, PROF_TWICE_PROJECT, PROF_EVENTS_TARGET = 1, 2, 4, 8
 
     def profile(self, enable=True) -> None:
         """True / False: per-phase event regions; an int: the STCA_PROF_* bit mask (include/stca.h)."""

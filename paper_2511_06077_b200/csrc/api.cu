@@ -170,7 +170,7 @@ struct stca_handle {
   int cap_layer = 0;
   void *cap_U = nullptr, *cap_Y = nullptr;
   // stca_profile
-  bool prof = false;
+  bool prof = false, prof_target = false;
   int reps_attn = 1, reps_proj = 1;  // STCA_PROF_TWICE_*
   std::vector<ProfRegion> prof_open;  // recorded, not yet read
   std::vector<cudaEvent_t> prof_pool;
@@ -1054,7 +1054,7 @@ static stca_status ffn_rows(stca_handle *h, const void *in, int64_t ldi, int64_t
   if (rows <= 0) return STCA_OK;
   if (h->bf16) {
     CU(h->hbuf.ensure((size_t)rows * rd * 2, st));  // H scratch owned by this handle
-    cudaEvent_t pa = prof_begin(h, st);
+    cudaEvent_t pa = h->prof_target ? prof_begin(h, st) : nullptr;
     CU(stca::tc_ffn(in, ldi, rows, which == 0 ? tcw->W1h : tcw->W1q, which == 0 ? tcw->Woh : tcw->Woq, d, rd, g, b,
                     h->cfg.ln_eps, out_s, ldo, out_f, ldof, h->hbuf.p, st));
     prof_end(h, STCA_PH_TARGET, pa, st);
@@ -1079,7 +1079,7 @@ static stca_status gemm(stca_handle *h, const void *A, int64_t lda, const void *
                         void *Cs, int64_t ldcs, float *Cf, int64_t ldcf, int64_t M, int N, int K, cudaStream_t st) {
   if (M <= 0) return STCA_OK;
   if (h->bf16) {
-    cudaEvent_t pa = prof_begin(h, st);
+    cudaEvent_t pa = h->prof_target ? prof_begin(h, st) : nullptr;
     CU(stca::tc_gemm(A, lda, Btc, M, N, K, Cs, ldcs, Cf, ldcf, st));
     prof_end(h, STCA_PH_TARGET, pa, st);
     return STCA_OK;
@@ -1182,14 +1182,24 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
   const bool tc_attn = h->bf16 && stca::tc_attention_supported(d);
+  // d = 256 / 512: the single-CTA M = 64 kernel (tc_attn_wide.cu).  The CTA-pair kernel (tc_attn_pair.cu,
+  // M = 128 per pair at full MMA rate) measured slower -- its SS A operand (U) is re-read from shared
+  // memory for every 64-key tile, so it is shared-memory-bandwidth bound; it is built only
+  // for A/B runs (-DSTCA_PAIR_ATTN).
+#ifdef STCA_PAIR_ATTN
+  const bool tc_wide = h->bf16 && stca::tc_attention_pair_supported(d);
+  const int wide_qtile = 128;
+#else
   const bool tc_wide = h->bf16 && stca::tc_attention_wide_supported(d);
+  const int wide_qtile = 64;
+#endif
   // A request with at most 64 query rows (m_b h) takes the transposed kernel (keys = MMA rows), which
   // does not pad it to a 128-row query tile.  The choice is PER REQUEST (its items are moved behind
   // the others and launched separately), so a request's arithmetic never depends on its batch
   // (RLB invariance, P10).  STCA_NO_NARROW=1 disables it (A/B runs).
   static const bool no_narrow = getenv("STCA_NO_NARROW") && atoi(getenv("STCA_NO_NARROW")) != 0;
   const bool tc_narrow = tc_attn && !no_narrow;
-  const int qtile = tc_attn ? 128 : tc_wide ? 64 : 16;
+  const int qtile = tc_attn ? 128 : tc_wide ? wide_qtile : 16;
   std::vector<int64_t> it6;
   int64_t nit = stca_plan_attention(h->len.data(), tgt_off, B, hh, qtile, (int32_t)h->chunk_cap, nullptr, 0);
   it6.resize((size_t)std::max<int64_t>(nit, 1) * 6);
@@ -1302,8 +1312,13 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
         CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
                             h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
     } else if (tc_wide) {
+#ifdef STCA_PAIR_ATTN
+      CU(stca::tc_attention_pair(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
+                                 h->part.as<float>(), st));
+#else
       CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
                                  h->part.as<float>(), st));
+#endif
     } else {
       CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
     }
@@ -1360,6 +1375,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
 extern "C" stca_status stca_profile(stca_handle *h, int32_t enable) {
   if (!h) return STCA_ERR_INVALID_ARG;
   h->prof = (enable & STCA_PROF_EVENTS) != 0;
+  h->prof_target = h->prof && (enable & STCA_PROF_EVENTS_TARGET) != 0;
   h->reps_attn = (enable & STCA_PROF_TWICE_ATTENTION) ? 2 : 1;
   h->reps_proj = (enable & STCA_PROF_TWICE_PROJECT) ? 2 : 1;
   return STCA_OK;

@@ -70,6 +70,10 @@ cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64
                                 const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
                                 cudaStream_t st);
 bool tc_attention_wide_supported(int d);
+// d in {256, 512}: CTA pairs (cta_group::2, M = 128 = 64 query rows per CTA), items of <= 128 query rows
+bool tc_attention_pair_supported(int d);
+cudaError_t tc_attention_pair(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
+                              int64_t n_items, int d, void *Y, float *part, cudaStream_t st);
 cudaError_t tc_attention_wide(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                               int64_t n_items, int d, void *Y, float *part, cudaStream_t st);
 // d = 128, persistent: CTA c processes items[cta_items[cta_off[c] .. cta_off[c+1])] in order

@@ -30,6 +30,9 @@
 #ifndef STCA_WIDE_LAZY
 #define STCA_WIDE_LAZY 8.f  // rescale threshold in log2 units (a test build sets 0: rescale on every increase)
 #endif
+#ifndef STCA_WIDE_PF
+#define STCA_WIDE_PF 4  // key tiles prefetched into L2 ahead of the TMA loads (0: off)
+#endif
 
 namespace stca {
 namespace tc {
@@ -96,7 +99,14 @@ __global__ void __launch_bounds__(352, 1)
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer: the key tiles, once ----------------
       int s = 0, ph = 0;
+      auto prefetch = [&](int j) {
+        if (j >= nt) return;
+#pragma unroll
+        for (int bx = 0; bx < D / 64; ++bx) tma_prefetch_l2(&mapX, 64 * bx, (int32_t)(it.key0 + (int64_t)j * C::BN));
+      };
+      for (int j = 0; j < STCA_WIDE_PF; ++j) prefetch(j);
       for (int j = 0; j < nt; ++j) {
+        if (STCA_WIDE_PF > 0) prefetch(j + STCA_WIDE_PF);
         mbar_wait(&x_empty[s], ph ^ 1);
         uint8_t *dst = sX + s * C::X_BYTES;
         const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BN);

@@ -122,12 +122,16 @@ def test_profiler_regions_and_allocators(allocator):
     wl = workload.make_workload(make_cfg(B=3, m=16, M=3), seed=8, lengths=np.array([9000, 100, 3000]))
     ref = run_gpu(wl)
     m = _model(wl, allocator=allocator)
-    m.profile(True)
+    m.profile(m.PROF_EVENTS | m.PROF_EVENTS_TARGET)
     Z, z = run_gpu(wl, model=m)
     p = m.profile_read()
     assert p["project"][1] == 1 and p["forward"][1] == 1, p
     assert p["attention"][1] == wl.cfg.M and p["merge"][1] == wl.cfg.M, p  # the 9000-key history is split
     assert p["target"][1] >= 2 * wl.cfg.M, p
+    m.profile(True)  # without target regions
+    run_gpu(wl, model=m)
+    p = m.profile_read()
+    assert p["target"][1] == 0 and p["attention"][1] == wl.cfg.M, p
     assert all(v[0] > 0 for k, v in p.items() if v[1]), p
     assert p["forward"][0] >= p["attention"][0], p
     assert np.array_equal(Z, ref[0]) and np.array_equal(z, ref[1])
