@@ -203,14 +203,14 @@ def lib_sha256():
     return h.hexdigest()
 
 
-def traffic_for(config, kernel):
-    """ncu DRAM bytes per launch for `kernel` at `config`, from profiles/traffic_r2.json -- only if that
-    capture was taken of THIS library build (sha256), else None."""
-    tf = os.path.join(ROOT, "profiles", "traffic_r2.json")
+def ncu_for(config, kernel):
+    """The committed ncu launch-list summary (profiles/ncu_r2.json, tools/ncu_summary.py) of `kernel` at
+    `config` -- only if that capture ran THIS library build (sha256), else None."""
+    tf = os.path.join(ROOT, "profiles", "ncu_r2.json")
     try:
-        t = json.load(open(tf)).get(config, {}).get(kernel)
-        if t and t.get("lib_sha256") == lib_sha256():
-            return t.get("dram_bytes_per_launch")
+        t = json.load(open(tf)).get(config, {})
+        if t.get("lib_sha256") == lib_sha256():
+            return dict(t.get(kernel, {}), source=t.get("source"))
     except Exception:
         pass
     return None
@@ -223,12 +223,22 @@ def roofline_entry(name, kernel, flops, bytes_, ms, pk, peak_kind, config):
     bw_peak = pk["hbm_gbs"]
     ridge = tf_peak * 1e12 / (bw_peak * 1e9)
     intensity = flops / bytes_ if bytes_ else float("inf")
-    if intensity >= ridge:
-        achieved, peak, unit, bound = flops / (ms * 1e-3) / 1e12, tf_peak, "TFLOP/s", "tensor"
-    else:
-        achieved, peak, unit, bound = bytes_ / (ms * 1e-3) / 1e9, bw_peak, "GB/s", "hbm"
+    tensor = intensity >= ridge
+
+    def rate(t_ms):
+        return flops / (t_ms * 1e-3) / 1e12 if tensor else bytes_ / (t_ms * 1e-3) / 1e9
+    achieved = rate(ms)
+    peak, unit, bound = (tf_peak, "TFLOP/s", "tensor") if tensor else (bw_peak, "GB/s", "hbm")
+    nc = ncu_for(config, kernel)
+    traffic = ncu_ms = None
+    if nc and nc.get("ms_per_launch"):
+        traffic = nc["dram_bytes_read_per_launch"] + nc["dram_bytes_write_per_launch"]
+        ncu_ms = nc["ms_per_launch"]
     return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": traffic_for(config, kernel),
+            "frac": achieved / peak, "traffic": traffic,
+            "ncu": None if ncu_ms is None else {"ms_per_launch": ncu_ms, "achieved": rate(ncu_ms),
+                                                "frac": rate(ncu_ms) / peak, "source": nc.get("source"),
+                                                "note": "cold-cache, serialised launch list of this build"},
             "peak_kind": f"measured {peak_kind} (MEASURED_PEAKS.json)" + (" (fallback)" if pk.get("_fallback") else ""),
             "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
             "intensity_flop_per_byte": intensity, "ridge": ridge, "ms_per_launch": ms}

@@ -89,7 +89,7 @@ struct HostPinned {
     p = nullptr;
     cap = 0;
     size_t want = bytes + bytes / 8 + 256;
-    cudaError_t e = cudaMallocHost(&p, want);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable);  // read by kernels too
     if (e == cudaSuccess) cap = want;
     return e;
   }
@@ -156,7 +156,7 @@ struct stca_handle {
   DevBuf xt_cache;  // M x [T2 x d] storage
   DevBuf xin[2], xgather, seg, proj_h, proj_y;  // xin: double-buffered host-input staging
   // forward scratch
-  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, items, mitems, ctal, zout, Zout;
+  DevBuf xtin, ocat, q, c, hbuf, ybuf32, U, Y, part, partg, plan, zout, Zout;  // plan: [items | merge items | CTA lists]
   StagingRing stage;
   // session cache (stca_session_open / stca_project_history_session): X~ rows per user across calls
   struct SessEntry {
@@ -178,6 +178,7 @@ struct stca_handle {
   // pipelined host-input projection: copy stream + one event per piece
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_xin_free[2] = {}, ev[STCA_H2D_PIECES] = {};
+  cudaEvent_t ev_xtin_free = nullptr, ev_xt_in = nullptr;  // host x_t upload on the copy stream
   int xin_k = 0;  // staging buffer of the next host-input projection
 };
 
@@ -185,7 +186,7 @@ static DevBuf *const *all_bufs(stca_handle *h, int *n) {
   static thread_local DevBuf *v[32];
   DevBuf *list[] = {&h->xt_cache, &h->xin[0], &h->xin[1], &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
-                    &h->part,     &h->partg, &h->items,  &h->mitems, &h->ctal,   &h->zout,   &h->Zout};
+                    &h->part,     &h->partg, &h->plan,   &h->zout,   &h->Zout};
   *n = (int)(sizeof list / sizeof list[0]);
   for (int i = 0; i < *n; ++i) v[i] = list[i];
   return v;
@@ -679,6 +680,8 @@ extern "C" void stca_destroy(stca_handle *h) {
   if (h->copy_st) {
     cudaStreamDestroy(h->copy_st);
     for (cudaEvent_t e : h->ev_xin_free) cudaEventDestroy(e);
+    cudaEventDestroy(h->ev_xtin_free);
+    cudaEventDestroy(h->ev_xt_in);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   }
   cudaGetLastError();
@@ -687,8 +690,8 @@ extern "C" void stca_destroy(stca_handle *h) {
 
 extern "C" const char *stca_last_error(const stca_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
-// A pinned staging slot of at least `bytes` bytes for host -> device copies enqueued on `st`; the
-// caller records *ev on `st` after its copies.  Waits only if the slot's previous copy is unfinished.
+// A pinned (host-mapped) staging slot of at least `bytes` bytes for uploads enqueued on `st`; the
+// caller records *ev on `st` after the upload.  Waits only if the slot's previous upload is unfinished.
 static stca_status staging_acquire(stca_handle *h, size_t bytes, void **out, cudaEvent_t *ev) {
   StagingRing &r = h->stage;
   const int k = r.next;
@@ -706,6 +709,38 @@ static stca_status staging_acquire(stca_handle *h, size_t bytes, void **out, cud
 // ===========================================================================
 // a1: X~(i) = LN(SwiGLUFFN(i)(X)) for all layers, Eq.(2), for cache rows [r0, r0 + rows) (X points at
 // row r0 of the compacted input)
+// The handle's copy stream for host inputs (created on first use; its "buffer free" events are
+// recorded on `st` right away, so the first uploads wait for every earlier reader on `st`).
+static stca_status ensure_copy_stream(stca_handle *h, cudaStream_t st) {
+  if (h->copy_st) return STCA_OK;
+  CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+  for (cudaEvent_t &e : h->ev_xin_free) {
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaEventRecord(e, st));
+  }
+  CU(cudaEventCreateWithFlags(&h->ev_xtin_free, cudaEventDisableTiming));
+  CU(cudaEventRecord(h->ev_xtin_free, st));
+  CU(cudaEventCreateWithFlags(&h->ev_xt_in, cudaEventDisableTiming));
+  for (cudaEvent_t &e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return STCA_OK;
+}
+
+// Host plan -> device buffer `dst` through a staging slot and a fetch kernel on `st` (SM loads of
+// mapped pinned memory): never queued behind a large host-input copy in the H2D copy engine.
+static stca_status upload_plan(stca_handle *h, const void *src, size_t bytes, DevBuf &dst, cudaStream_t st) {
+  const size_t b16 = (bytes + 15) / 16 * 16;
+  CU(dst.ensure(b16 + 64, st));
+  if (!bytes) return STCA_OK;
+  void *slot = nullptr;
+  cudaEvent_t slot_ev = nullptr;
+  stca_status s = staging_acquire(h, b16, &slot, &slot_ev);
+  if (s != STCA_OK) return s;
+  memcpy(slot, src, bytes);
+  CU(stca::fetch_mapped(slot, dst.p, b16, st));
+  CU(cudaEventRecord(slot_ev, st));
+  return STCA_OK;
+}
+
 static stca_status project_rows(stca_handle *h, const void *X, int64_t r0, int64_t rows, cudaStream_t st) {
   const int d = h->cfg.d, M = h->cfg.M, rd = h->cfg.r * d, es = h->es;
   const size_t row_bytes = (size_t)d * es;
@@ -819,14 +854,8 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
   if (host_x && !gather && T2 > 0) {
     // host input, no gather: stream X up in pieces on a copy stream and project each piece as soon as
     // it has landed, so the H2D copy (the e2e bottleneck) overlaps the projection of earlier pieces
-    if (!h->copy_st) {
-      CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
-      for (cudaEvent_t &e : h->ev_xin_free) {  // recorded now: uploads wait for every earlier reader on `stream`
-        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CU(cudaEventRecord(e, st));
-      }
-      for (cudaEvent_t &e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    stca_status cs = ensure_copy_stream(h, st);
+    if (cs != STCA_OK) return cs;
     // two staging buffers in turn: the upload of call n + 1 waits only for the projection of call n - 1
     // (its buffer's last reader), so the PCIe copies of consecutive calls run back to back
     const int xk = h->xin_k;
@@ -870,14 +899,8 @@ extern "C" stca_status stca_project_history(stca_handle *h, const void *X, int64
       seg.push_back(h->olen[b]);
       maxlen = std::max(maxlen, h->olen[b]);
     }
-    CU(h->seg.ensure(seg.size() * 8, st));
-    void *slot = nullptr;
-    cudaEvent_t slot_ev = nullptr;
-    stca_status ss = staging_acquire(h, seg.size() * 8, &slot, &slot_ev);
+    stca_status ss = upload_plan(h, seg.data(), seg.size() * 8, h->seg, st);
     if (ss != STCA_OK) return ss;
-    memcpy(slot, seg.data(), seg.size() * 8);
-    CU(cudaMemcpyAsync(h->seg.p, slot, seg.size() * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaEventRecord(slot_ev, st));
     CU(h->xgather.ensure((size_t)T2 * row_bytes, st));
     CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), B, maxlen, (int)row_bytes, st));
     Xd = h->xgather.p;
@@ -1024,14 +1047,8 @@ extern "C" stca_status stca_project_history_session(stca_handle *h, const int64_
       dst += len[b];
       maxlen = std::max(maxlen, len[b]);
     }
-    CU(h->seg.ensure(seg.size() * 8, st));
-    void *slot = nullptr;
-    cudaEvent_t slot_ev = nullptr;
-    s = staging_acquire(h, seg.size() * 8, &slot, &slot_ev);
+    s = upload_plan(h, seg.data(), seg.size() * 8, h->seg, st);
     if (s != STCA_OK) return s;
-    memcpy(slot, seg.data(), seg.size() * 8);
-    CU(cudaMemcpyAsync(h->seg.p, slot, seg.size() * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaEventRecord(slot_ev, st));
     CU(h->xgather.ensure((size_t)R * row_bytes, st));
     CU(stca::gather_rows(Xd, h->xgather.p, h->seg.as<int64_t>(), (int64_t)miss.size(), maxlen, (int)row_bytes, st));
     s = project_rows(h, h->xgather.p, a, R, st);
@@ -1158,9 +1175,17 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
 
   // inputs: x_t into block 0 of the concatenation buffer [x_t | o1 | ... | oM] (R10)
   const void *xtd = xt;
-  if (!is_device_ptr(xt)) {
+  const bool host_xt = !is_device_ptr(xt);
+  if (host_xt) {  // on the copy stream, behind this step's history upload (the H2D engine is FIFO)
+    s = ensure_copy_stream(h, st);
+    if (s != STCA_OK) return s;
+    void *const old = h->xtin.p;
     CU(h->xtin.ensure((size_t)Nt * d * es, st));
-    CU(cudaMemcpyAsync(h->xtin.p, xt, (size_t)Nt * d * es, cudaMemcpyHostToDevice, st));
+    if (h->xtin.p != old) CU(cudaEventRecord(h->ev_xtin_free, st));
+    CU(cudaStreamWaitEvent(h->copy_st, h->ev_xtin_free, 0));  // the previous forward has read x_t
+    CU(cudaMemcpyAsync(h->xtin.p, xt, (size_t)Nt * d * es, cudaMemcpyHostToDevice, h->copy_st));
+    CU(cudaEventRecord(h->ev_xt_in, h->copy_st));
+    CU(cudaStreamWaitEvent(st, h->ev_xt_in, 0));
     xtd = h->xtin.p;
   }
   float *Zd = out_Z, *zd = out_z;
@@ -1179,6 +1204,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
   CU(h->U.ensure((size_t)NQ * d * es, st));
   CU(h->Y.ensure((size_t)NQ * d * es, st));
   CU(stca::copy_rows_strided(xtd, (int64_t)d * es, h->ocat.p, ldo * es, Nt, d * es, st));
+  if (host_xt) CU(cudaEventRecord(h->ev_xtin_free, st));
 
   // attention plan (host, exact): items in LPT order, partial rows for multi-chunk requests
   const bool tc_attn = h->bf16 && stca::tc_attention_supported(d);
@@ -1266,26 +1292,21 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     stca_plan_persistent(cost.data(), nit_nar, n_ctas_nar, ctal_resize(v, n_ctas_nar, nit_nar), bin.data());
     ctal.insert(ctal.end(), v.begin(), v.end());
   }
+  // the plan [items | merge items | CTA lists], 256-byte aligned sections, in one upload
   const size_t items_bytes = items.size() * sizeof(stca::AttnItem), mi_bytes = mi.size() * sizeof(stca::MergeItem);
   const size_t ctal_bytes = ctal.size() * sizeof(int32_t);
-  CU(h->items.ensure(items_bytes + 64, st));
-  CU(h->mitems.ensure(mi_bytes + 64, st));
-  CU(h->ctal.ensure(ctal_bytes + 64, st));
-  {  // the plan reaches the device through a pinned staging slot: no host wait
-    void *slot = nullptr;
-    cudaEvent_t slot_ev = nullptr;
-    s = staging_acquire(h, items_bytes + mi_bytes + ctal_bytes + 64, &slot, &slot_ev);
+  const size_t mi_at = (items_bytes + 255) / 256 * 256, ctal_at = mi_at + (mi_bytes + 255) / 256 * 256;
+  {
+    std::vector<uint8_t> pl(ctal_at + ctal_bytes);
+    if (items_bytes) memcpy(pl.data(), items.data(), items_bytes);
+    if (mi_bytes) memcpy(pl.data() + mi_at, mi.data(), mi_bytes);
+    if (ctal_bytes) memcpy(pl.data() + ctal_at, ctal.data(), ctal_bytes);
+    s = upload_plan(h, pl.data(), pl.size(), h->plan, st);
     if (s != STCA_OK) return s;
-    uint8_t *pin = (uint8_t *)slot;
-    memcpy(pin, items.data(), items_bytes);
-    memcpy(pin + items_bytes, mi.data(), mi_bytes);
-    memcpy(pin + items_bytes + mi_bytes, ctal.data(), ctal_bytes);
-    if (items_bytes) CU(cudaMemcpyAsync(h->items.p, pin, items_bytes, cudaMemcpyHostToDevice, st));
-    if (mi_bytes) CU(cudaMemcpyAsync(h->mitems.p, pin + items_bytes, mi_bytes, cudaMemcpyHostToDevice, st));
-    if (ctal_bytes)
-      CU(cudaMemcpyAsync(h->ctal.p, pin + items_bytes + mi_bytes, ctal_bytes, cudaMemcpyHostToDevice, st));
-    CU(cudaEventRecord(slot_ev, st));
   }
+  stca::AttnItem *d_items = h->plan.as<stca::AttnItem>();
+  stca::MergeItem *d_mitems = reinterpret_cast<stca::MergeItem *>(h->plan.as<uint8_t>() + mi_at);
+  int32_t *d_ctal = reinterpret_cast<int32_t *>(h->plan.as<uint8_t>() + ctal_at);
   const size_t part_bytes = (size_t)part_rows * stca::part_row_bytes(d, es);
   if (part_rows) CU(h->part.ensure(part_bytes, st));
   if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G, st));
@@ -1305,22 +1326,22 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     for (int rep = 0; rep < h->reps_attn; ++rep) {  // idempotent (STCA_PROF_TWICE_ATTENTION)
     if (tc_attn) {
       if (nit_nar > 0)
-        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>() + nit_reg,
-                                     h->ctal.as<int32_t>() + nar_at, h->ctal.as<int32_t>() + nar_at + n_ctas_nar + 1,
+        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, d_items + nit_reg,
+                                     d_ctal + nar_at, d_ctal + nar_at + n_ctas_nar + 1,
                                      n_ctas_nar, h->Y.p, h->part.as<float>(), st));
       if (nit_reg > 0)
-        CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), h->ctal.as<int32_t>(),
-                            h->ctal.as<int32_t>() + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
+        CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, d_items, d_ctal,
+                            d_ctal + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
     } else if (tc_wide) {
 #ifdef STCA_PAIR_ATTN
-      CU(stca::tc_attention_pair(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
+      CU(stca::tc_attention_pair(h->U.p, NQ, Xt, h->T2, d_items, nit, d, h->Y.p,
                                  h->part.as<float>(), st));
 #else
-      CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, h->items.as<stca::AttnItem>(), nit, d, h->Y.p,
+      CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, d_items, nit, d, h->Y.p,
                                  h->part.as<float>(), st));
 #endif
     } else {
-      CU(stca::cc_attention(h->bf16, h->U.p, Xt, h->items.as<stca::AttnItem>(), nit, d, h->Y.p, h->part.as<float>(), st));
+      CU(stca::cc_attention(h->bf16, h->U.p, Xt, d_items, nit, d, h->Y.p, h->part.as<float>(), st));
     }
     }
     prof_end(h, STCA_PH_ATTENTION, pa, st);
@@ -1334,7 +1355,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       CU(cudaMemcpyAsync(h->cap_U, h->U.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
     }
     pa = prof_begin(h, st);
-    CU(stca::merge_partials(h->bf16, h->mitems.as<stca::MergeItem>(), (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
+    CU(stca::merge_partials(h->bf16, d_mitems, (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
                             G, (int64_t)part_bytes, h->Y.p, st));
     if (!mi.empty()) prof_end(h, STCA_PH_MERGE, pa, st);
     else if (pa) h->prof_pool.push_back(pa);

@@ -387,6 +387,24 @@ cudaError_t copy_rows_strided(const void *src, int64_t lds, void *dst, int64_t l
   return cudaGetLastError();
 }
 
+// host-mapped pinned memory -> device, by SM loads over PCIe (no copy engine: a plan upload must not
+// queue behind a large host-input copy in the H2D engine)
+__global__ void k_fetch_mapped(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int64_t n16) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t fetch_mapped(const void *src_mapped, void *dst, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  if ((bytes | (uintptr_t)src_mapped | (uintptr_t)dst) % 16) return cudaErrorInvalidValue;
+  const int64_t n16 = (int64_t)(bytes / 16);
+  unsigned g = (unsigned)((n16 + 255) / 256);
+  if (g > 64) g = 64;
+  note_launch();
+  k_fetch_mapped<<<g, 256, 0, st>>>((const uint4 *)src_mapped, (uint4 *)dst, n16);
+  return cudaGetLastError();
+}
+
 __global__ void k_f32_to_bf16(const float *__restrict__ s, bf16 *__restrict__ t, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     t[i] = __float2bfloat16_rn(s[i]);

@@ -65,6 +65,8 @@ cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg /*[n][3]:
 cudaError_t copy_rows_strided(const void *src, int64_t lds, void *dst, int64_t ldd, int64_t rows, int row_bytes,
                               cudaStream_t st);
 cudaError_t f32_to_bf16(const float *src, bf16 *dst, int64_t n, cudaStream_t st);
+// bytes (multiple of 16, 16-byte aligned) from host-mapped pinned memory to device memory by a kernel
+cudaError_t fetch_mapped(const void *src_mapped, void *dst, size_t bytes, cudaStream_t st);
 cudaError_t bf16_to_f32(const bf16 *src, float *dst, int64_t n, cudaStream_t st);
 // WQK[e][r*d+f] = scale * sum_c WQ[e][r dh + c] WK[f][r dh + c];  WVO[r*d+e][f] = sum_c WV[e][r dh+c] WO[r dh+c][f]
 cudaError_t prep_qk_vo(const float *WQ, const float *WK, const float *WV, const float *WO, int d, int h,
