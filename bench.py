@@ -276,8 +276,19 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-            os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line (NCCL prints its version otherwise)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            os.environ["NCCL_DEBUG"] = "WARN"
+        # stdout carries exactly one JSON line: NCCL's version banner goes to stderr (fd 1 -> fd 2 while
+        # the communicator is created)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     # split1 (BASELINE config 5): ONE L = 10k history split over the ranks (split-history, one all-gather
     # of partials per layer); every other config: the same global request set on every rank, LPT-sharded
     split = args.config == "split1"

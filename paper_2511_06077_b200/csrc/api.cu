@@ -1311,16 +1311,49 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
   if (part_rows) CU(h->part.ensure(part_bytes, st));
   if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G, st));
 
+  // target side: at d = 128 every layer boundary is ONE fused kernel (tc_chain.cu: o(i) -> Z, ocat;
+  // c = [..] W_C; q = SwiGLUFFN(c); U = q W_QK), otherwise separate tcgen05 GEMMs / CUDA-core kernels
+#ifdef STCA_NO_CHAIN  // A/B builds only: the separate-GEMM target side
+  const bool chain = false;
+#else
+  const bool chain = h->bf16 && stca::tc_chain_supported(d, hh, h->cfg.r * d);
+#endif
+  auto chain_base = [&](int mode) {
+    stca::TcChain c;
+    c.mode = mode;
+    c.M = M;
+    c.h = hh;
+    c.rd = h->cfg.r * d;
+    c.Nt = Nt;
+    c.ocat = h->ocat.p;
+    c.U = h->U.p;
+    c.eps = h->cfg.ln_eps;
+    return c;
+  };
   // a2: q(1) = LN(SwiGLUFFN(1)(x_t)), Eq.(3)
   LayerW &L1 = h->L[0];
-  s = ffn_rows(h, h->ocat.p, ldo, Nt, L1.W1q, L1.Woq, &L1.tc, 1, L1.gq, L1.bq, h->q.p, d, nullptr, 0, st);
-  if (s != STCA_OK) return s;
+  if (chain) {  // ... and a3 of layer 1
+    stca::TcChain c = chain_base(0);
+    c.W1t = L1.tc.W1q;
+    c.Wot = L1.tc.Woq;
+    c.WQKt = L1.tc.WQK;
+    c.g = L1.gq;
+    c.b = L1.bq;
+    cudaEvent_t pa = h->prof_target ? prof_begin(h, st) : nullptr;
+    CU(stca::tc_chain(c, st));
+    prof_end(h, STCA_PH_TARGET, pa, st);
+  } else {
+    s = ffn_rows(h, h->ocat.p, ldo, Nt, L1.W1q, L1.Woq, &L1.tc, 1, L1.gq, L1.bq, h->q.p, d, nullptr, 0, st);
+    if (s != STCA_OK) return s;
+  }
   for (int i = 1; i <= M; ++i) {
     LayerW &Ly = h->L[i - 1];
     const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)(i - 1) * h->T2 * d * es;
-    // a3: U = q W_QK (all heads; pre-scaled by log2(e)/sqrt(d_h)) -> [Nt h x d]
-    s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
-    if (s != STCA_OK) return s;
+    // a3: U = q W_QK (all heads; pre-scaled by log2(e)/sqrt(d_h)) -> [Nt h x d] (fused: by the previous chain)
+    if (!chain) {
+      s = gemm(h, h->q.p, d, Ly.WQK, Ly.tc.WQK, (int64_t)hh * d, h->U.p, (int64_t)hh * d, nullptr, 0, Nt, hh * d, d, st);
+      if (s != STCA_OK) return s;
+    }
     // a4: ragged single-query attention per request, reordered form Eq.(13)
     cudaEvent_t pa = prof_begin(h, st);
     for (int rep = 0; rep < h->reps_attn; ++rep) {  // idempotent (STCA_PROF_TWICE_ATTENTION)
@@ -1363,6 +1396,32 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       CU(cudaMemcpyAsync(h->cap_Y, h->Y.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
       h->cap_layer = 0;
     }
+    if (chain) {  // a5 (+ a6, a3 of layer i + 1; or a7 after the last layer) as one kernel
+      stca::TcChain c = chain_base(i < M ? 1 : 2);
+      c.Y = h->Y.p;
+      c.ocat_out = (uint8_t *)h->ocat.p + (size_t)i * d * es;
+      c.Z = Zd + (size_t)(i - 1) * d;
+      c.ldz = (int64_t)M * d;
+      c.WVOt = Ly.tc.WVO;
+      if (i < M) {
+        LayerW &Ln = h->L[i];
+        c.kc = i + 1;
+        c.WCt = Ln.tc.WC;
+        c.W1t = Ln.tc.W1q;
+        c.Wot = Ln.tc.Woq;
+        c.WQKt = Ln.tc.WQK;
+      } else if (zd) {
+        c.kc = M + 1;
+        c.WCt = h->tcz.WC;
+        c.W1t = h->tcz.W1h;
+        c.Wot = h->tcz.Woh;
+        c.zout = zd;
+      }
+      cudaEvent_t pa = h->prof_target ? prof_begin(h, st) : nullptr;
+      CU(stca::tc_chain(c, st));
+      prof_end(h, STCA_PH_TARGET, pa, st);
+      continue;
+    }
     // a5: o(i) = [Y_r]_r W_VO -> out_Z[:, i] (fp32) and block i of the concatenation (storage)
     s = gemm(h, h->Y.p, (int64_t)hh * d, Ly.WVO, Ly.tc.WVO, d, (uint8_t *)h->ocat.p + (size_t)i * d * es, ldo,
              Zd + (size_t)(i - 1) * d, (int64_t)M * d, Nt, d, hh * d, st);
@@ -1376,8 +1435,8 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       if (s != STCA_OK) return s;
     }
   }
-  // a7: z = SwiGLUFFN_Z([o(1)..o(M) | x_t] W_Z), Eq.(9)
-  if (zd) {
+  // a7: z = SwiGLUFFN_Z([o(1)..o(M) | x_t] W_Z), Eq.(9) (fused: by the last chain)
+  if (zd && !chain) {
     s = gemm(h, h->ocat.p, ldo, h->WZ, h->tcz.WC, d, h->c.p, d, nullptr, 0, Nt, d, (M + 1) * d, st);
     if (s != STCA_OK) return s;
     s = ffn_rows(h, h->c.p, d, Nt, h->W1z, h->Woz, &h->tcz, 0, nullptr, nullptr, nullptr, 0, zd, d, st);

@@ -4,6 +4,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// STCA_DEBUG_SYNC builds: device-side invariant checks that trap with the failed condition (see
+// mbar_wait in tc_ptx.cuh); compiled out otherwise.
+#ifdef STCA_DEBUG_SYNC
+#include <stdio.h>
+#define STCA_DCHECK(cond)                                                                                  \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("STCA_DEBUG_SYNC check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x);                                                           \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define STCA_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace stca {
 
 typedef __nv_bfloat16 bf16;

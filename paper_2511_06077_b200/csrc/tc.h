@@ -70,6 +70,26 @@ cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64
                                 const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
                                 cudaStream_t st);
 bool tc_attention_wide_supported(int d);
+// The target-side update of one layer boundary as ONE kernel (d = 128; tc_chain.cu):
+//   mode 0 (first): q(1) = LN(SwiGLUFFN(x_t)) -> U(1);  1 (mid): o(i) -> Z, ocat; c = ocat[:, :(i+1)d] W_C;
+//   q = SwiGLUFFN(c) -> U(i+1);  2 (last): o(M) -> Z, ocat (and z = SwiGLUFFN_Z(ocat W_Z) if zout)
+struct TcChain {
+  int mode = 0, M = 0, h = 0, rd = 0;
+  int64_t Nt = 0;
+  int kc = 0;                      // K blocks of d of the c GEMM: i + 1 (mid), M + 1 (last with z)
+  const void *Y = nullptr;         // [Nt x h d] bf16 (mid / last)
+  const void *ocat = nullptr;      // [Nt x (M+1) d] bf16, read (x_t, earlier o)
+  void *ocat_out = nullptr;        // ocat + i d: where o(i) goes
+  float *Z = nullptr;              // out_Z + (i-1) d
+  int64_t ldz = 0;
+  void *U = nullptr;               // [Nt x h d] bf16 out (first / mid)
+  float *zout = nullptr;           // [Nt x d] fp32 (last, with z)
+  const void *WVOt = nullptr, *WCt = nullptr, *W1t = nullptr, *Wot = nullptr, *WQKt = nullptr;
+  const float *g = nullptr, *b = nullptr;
+  float eps = 1e-5f;
+};
+bool tc_chain_supported(int d, int h, int rd);
+cudaError_t tc_chain(const TcChain &c, cudaStream_t st);
 // d in {256, 512}: CTA pairs (cta_group::2, M = 128 = 64 query rows per CTA), items of <= 128 query rows
 bool tc_attention_pair_supported(int d);
 cudaError_t tc_attention_pair(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       for (int k = 0; k < STCA_ATTN_PF; ++k) pf_step();
       for (int k = 0; k < ni; ++k) {
         const AttnItem it = item(k);
+        STCA_DCHECK(it.klen >= 1 && it.nq >= 1 && it.nq <= AT_BM && it.key0 >= 0 && it.qrow0 >= 0);
         // U of item k into the staging area once the softmax warps moved U(k-1) into TMEM and the
         // epilogue of item k-2 (which staged its output there) is done; both are one us_free phase
         if (k >= 1) mbar_wait(us_free, (k - 1) & 1);

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
       for (int k = 0; k < STCA_NARROW_PF; ++k) pf_step();
       for (int n = i0; n < i1; ++n) {
         const AttnItem it = items[cta_items[n]];
+        STCA_DCHECK(it.klen >= 1 && it.nq >= 1 && it.nq <= C::NQ && it.key0 >= 0 && it.qrow0 >= 0);
         const int ni = n - i0, ub = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
         if (ni >= 2) mbar_wait(&u_free[ub], ((ni - 2) >> 1) & 1);
         mbar_expect_tx(&u_full[ub], C::U_BYTES);

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(352, 1)
   const AttnItem it = items[blockIdx.x];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nt = (it.klen + C::BN - 1) / C::BN;
+  STCA_DCHECK(it.klen >= 1 && it.nq >= 1 && it.nq <= C::BM && it.key0 >= 0 && it.qrow0 >= 0);
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&mapX);

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace stca {
 namespace tc {
@@ -40,10 +41,25 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
       : "memory");
   return ok;
 }
+// STCA_DEBUG_SYNC builds (the substitute for compute-sanitizer's synccheck, which this pool does not
+// run): a watchdog traps with the barrier's shared-memory offset, the awaited parity and the thread
+// instead of hanging when a phase never completes (a protocol bug: a missing arrive / commit or a
+// wrong phase), so a test fails loudly.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#ifdef STCA_DEBUG_SYNC
+  long long spins = 0;
+  while (!mbar_try_wait(a, parity)) {
+    if (++spins == (1ll << 26)) {
+      printf("STCA_DEBUG_SYNC: mbarrier 0x%x parity %u not completed (block %d, thread %d)\n", a, parity,
+             (int)blockIdx.x, (int)threadIdx.x);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(a, parity)) {
   }
+#endif
 }
 
 // ---------------- TMA ----------------

@@ -127,7 +127,7 @@ def test_profiler_regions_and_allocators(allocator):
     p = m.profile_read()
     assert p["project"][1] == 1 and p["forward"][1] == 1, p
     assert p["attention"][1] == wl.cfg.M and p["merge"][1] == wl.cfg.M, p  # the 9000-key history is split
-    assert p["target"][1] >= 2 * wl.cfg.M, p
+    assert p["target"][1] >= wl.cfg.M, p  # fused chain: M + 1 launches; separate GEMMs: more
     m.profile(True)  # without target regions
     run_gpu(wl, model=m)
     p = m.profile_read()
