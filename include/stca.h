@@ -256,6 +256,23 @@ stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const int64_t *hi
                              const int64_t *new_off, int64_t B, int32_t L_avg, void *P, int64_t *seg_off,
                              int64_t *segs, void *stream);
 
+/* ---- backward of one layer's attention (partial) ----
+ * PAPER.md Eq.(14) trains the stack end to end; RLB aggregates the gradients of a
+ * request's shared history before they leave the request.  For layer `layer` of the
+ * last projection (bf16 path, d = 128): given the forward's reordered queries U (DEVICE bf16 [N_t h x d],
+ * row t h + r, pre-scaled by log2(e)/sqrt(d_h); e.g. from the forward) and dY = dLoss/dY (DEVICE fp32
+ * [N_t h x d]), writes
+ *   dXt (DEVICE fp32 [T' x d], the X~ cache's compacted row order: request b's kept rows from its
+ *        offset, see stca_read_cache): dX~_b = alpha^T dY_b + dS^T U_b -- summed over ALL of the
+ *        request's target-head rows inside the kernel (rows of requests without targets: 0),
+ *   dU (DEVICE fp32 [N_t h x d]): dS X~_b,
+ * with alpha = softmax(ln 2 * U_b X~_b^T), D = rowsum(alpha (dY X~_b^T)), dS = ln 2 alpha (dY X~_b^T - D).
+ * A request with more than 64 target-head rows adds its blocks' dX~ with fp32 atomics (the last bits
+ * then depend on their order).  Asynchronous on `stream`.  STATE without a projection or for a B
+ * mismatch, UNSUPPORTED off the bf16 d = 128 path or in split-history mode, INVALID_ARG otherwise. */
+stca_status stca_attention_backward(stca_handle *h, int32_t layer, const void *U, const float *dY,
+                                    const int64_t *tgt_off, int64_t B, float *dXt, float *dU, void *stream);
+
 /* ---- input-encoding prologue ----
  * PAPER.md §3.1.1 "Input encoding" (video, action-type and position embeddings fused into x_j)
  * and the time-delta side information (request time minus item timestamp); additive fusion as

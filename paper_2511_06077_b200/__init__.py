@@ -189,6 +189,28 @@ class STCA:
                                                 off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
                                                 ctypes.c_void_p(_stream(stream))))
         self._B = B
+        self._T2 = None
+
+    def attention_backward(self, layer: int, U, dY, tgt_off, dXt=None, dU=None, stream=None):
+        """stca_attention_backward (NEXT-1, partial): (dXt [T' x d], dU [N_t h x d]) float32 CUDA tensors for
+        layer `layer` of the last projection, given its U (bf16 / int16 CUDA [N_t h x d]) and dY (float32)."""
+        import torch
+        off = _i64(tgt_off)
+        B = off.shape[0] - 1
+        if dXt is None:
+            dXt = torch.empty((self._cache_rows(), self.d), dtype=torch.float32, device=dY.device)
+        if dU is None:
+            dU = torch.empty_like(dY)
+        self._check(lib().stca_attention_backward(self._h, int(layer), ctypes.c_void_p(_ptr(U)), ctypes.c_void_p(_ptr(dY)),
+                                                  off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
+                                                  ctypes.c_void_p(_ptr(dXt)), ctypes.c_void_p(_ptr(dU)),
+                                                  ctypes.c_void_p(_stream(stream))))
+        return dXt, dU
+
+    def _cache_rows(self) -> int:
+        if getattr(self, "_T2", None) is None:
+            raise ValueError("pass dXt (the cache holds sum_b L'_b rows) or call project_history with track=True")
+        return self._T2
 
     def session_open(self, capacity_rows: int, stream=None) -> None:
         """Persistent per-user X~ cache (NEXT-4); see stca_session_open."""

@@ -1492,3 +1492,54 @@ extern "C" stca_status stca_debug_capture(stca_handle *h, int32_t layer, void *U
   h->cap_Y = Y_out;
   return STCA_OK;
 }
+
+// ===========================================================================
+// NEXT-1 (partial): backward of one layer's attention with request-level gradient aggregation
+// ===========================================================================
+extern "C" stca_status stca_attention_backward(stca_handle *h, int32_t layer, const void *U, const float *dY,
+                                               const int64_t *tgt_off, int64_t B, float *dXt, float *dU,
+                                               void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (h->B < 0) return fail(h, STCA_ERR_STATE, "stca_attention_backward before stca_project_history");
+  if (B != h->B) return fail(h, STCA_ERR_STATE, "B=%lld differs from the projected B=%lld", (long long)B, (long long)h->B);
+  if (!h->bf16 || h->cfg.d != 128)
+    return fail(h, STCA_ERR_UNSUPPORTED, "the attention backward runs on the bf16 path with d = 128 (d=%d)", h->cfg.d);
+  if (h->cfg.split_world > 1) return fail(h, STCA_ERR_UNSUPPORTED, "no attention backward in split-history mode");
+  if (layer < 1 || layer > h->cfg.M) return fail(h, STCA_ERR_INVALID_ARG, "layer %d outside 1..%d", layer, h->cfg.M);
+  if (!tgt_off) return fail(h, STCA_ERR_INVALID_ARG, "tgt_off is NULL");
+  const int64_t Nt = tgt_off[B];
+  int64_t badi = -1;
+  stca_status s = check_offsets(tgt_off, B, Nt, false, &badi);
+  if (s != STCA_OK) return fail(h, s, "tgt_off invalid at request %lld", (long long)badi);
+  if (Nt > 0 && (!U || !dY || !dU)) return fail(h, STCA_ERR_INVALID_ARG, "NULL U / dY / dU");
+  if (!dXt) return fail(h, STCA_ERR_INVALID_ARG, "dXt is NULL");
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = h->cfg.d, hh = h->cfg.h;
+  const int64_t NQ = Nt * hh;
+  // work items: (request, block of <= 64 query rows) over ALL of the request's kept keys
+  std::vector<stca::AttnItem> items;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
+    const int64_t nqb = (rows + 63) / 64;
+    for (int64_t qb = 0; qb < nqb; ++qb) {
+      stca::AttnItem a{};
+      a.qrow0 = tgt_off[b] * hh + 64 * qb;
+      a.nq = (int32_t)std::min<int64_t>(64, rows - 64 * qb);
+      a.key0 = h->coff[b];
+      a.klen = (int32_t)h->len[b];
+      a.chunk = 0;
+      a.part_row = nqb > 1 ? 1 : 0;  // several items add into the request's dX~ rows
+      items.push_back(a);
+    }
+  }
+  // dX~ rows of requests without targets (and the sums of multi-block requests) start from zero
+  CU(cudaMemsetAsync(dXt, 0, (size_t)h->T2 * d * sizeof(float), st));
+  if (items.empty()) return STCA_OK;
+  s = upload_plan(h, items.data(), items.size() * sizeof(stca::AttnItem), h->seg, st);
+  if (s != STCA_OK) return s;
+  const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)(layer - 1) * h->T2 * d * h->es;
+  CU(stca::tc_attention_bwd(U, NQ, Xt, h->T2, h->seg.as<stca::AttnItem>(), (int64_t)items.size(), dY, dXt, dU, st));
+  return STCA_OK;
+}

@@ -89,6 +89,10 @@ struct TcChain {
   float eps = 1e-5f;
 };
 bool tc_chain_supported(int d, int h, int rd);
+// NEXT-1 (partial): attention backward of one layer, d = 128; items of <= 64 query rows covering all of
+// a request's keys (part_row != 0: dX~ accumulated with fp32 reductions, else stored)
+cudaError_t tc_attention_bwd(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
+                             int64_t n_items, const float *dY, float *dX, float *dU, cudaStream_t st);
 cudaError_t tc_chain(const TcChain &c, cudaStream_t st);
 // d in {256, 512}: CTA pairs (cta_group::2, M = 128 = 64 query rows per CTA), items of <= 128 query rows
 bool tc_attention_pair_supported(int d);
