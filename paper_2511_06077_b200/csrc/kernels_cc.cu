@@ -130,6 +130,45 @@ cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float
 // log2(e)/sqrt(d_h)).  Writes normalised Y rows (single-chunk requests) or
 // (m, l, O) partials.
 // --------------------------------------------------------------------------
+// 16-byte (128-bit) loads of `n` storage elements at src -> fp32 in dst (n % (16 / sizeof(S)) == 0)
+template <typename S>
+__device__ __forceinline__ void unpack16(const uint4 v, float *dst) {
+  if constexpr (sizeof(S) == 2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      dst[2 * i] = __uint_as_float(w[i] << 16);
+      dst[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  } else {
+    dst[0] = __uint_as_float(v.x);
+    dst[1] = __uint_as_float(v.y);
+    dst[2] = __uint_as_float(v.z);
+    dst[3] = __uint_as_float(v.w);
+  }
+}
+
+// rows [r0, r0 + nr) of a row-major [* x d] storage matrix -> fp32 rows of stride dp in shared memory
+// (zero past `valid` rows); 128-bit coalesced loads when a row is a whole number of 16-byte chunks
+template <typename S>
+__device__ __forceinline__ void load_rows_f32(const S *__restrict__ src, int64_t r0, int nr, int valid, int d, float *dst,
+                                              int dp) {
+  constexpr int V = 16 / sizeof(S);
+  if (d % V == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int cpr = d / V;
+    for (int i = threadIdx.x; i < nr * cpr; i += blockDim.x) {
+      const int j = i / cpr, e = (i - j * cpr) * V;
+      const uint4 v = j < valid ? __ldg(reinterpret_cast<const uint4 *>(src + (r0 + j) * d + e)) : make_uint4(0, 0, 0, 0);
+      unpack16<S>(v, dst + j * dp + e);
+    }
+  } else {
+    for (int i = threadIdx.x; i < nr * d; i += blockDim.x) {
+      const int j = i / d, e = i % d;
+      dst[j * dp + e] = j < valid ? to_f(src[(r0 + j) * d + e]) : 0.f;
+    }
+  }
+}
+
 template <typename S>
 __global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, const S *__restrict__ Xt,
                                                       const AttnItem *__restrict__ items, int d,
@@ -140,10 +179,7 @@ __global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, c
   float *Us = sm;             // [16][dp]
   float *Xs = Us + 16 * dp;   // [32][dp]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < 16 * d; i += 256) {
-    int q = i / d, e = i % d;
-    Us[q * dp + e] = q < it.nq ? to_f(U[(it.qrow0 + q) * d + e]) : 0.f;
-  }
+  load_rows_f32(U, it.qrow0, 16, it.nq, d, Us, dp);
   const int nd = (d + 31) / 32;  // dims per lane (<= 16)
   float O[2][16];
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
@@ -154,10 +190,7 @@ __global__ void __launch_bounds__(256) k_cc_attention(const S *__restrict__ U, c
   for (int j0 = 0; j0 < it.klen; j0 += 32) {
     __syncthreads();
     const int nk = min(32, it.klen - j0);
-    for (int i = threadIdx.x; i < 32 * d; i += 256) {
-      int j = i / d, e = i % d;
-      Xs[j * dp + e] = j < nk ? to_f(Xt[(it.key0 + j0 + j) * d + e]) : 0.f;
-    }
+    load_rows_f32(Xt, it.key0 + j0, 32, nk, d, Xs, dp);
     __syncthreads();
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
