@@ -273,6 +273,21 @@ stca_status stca_rlb_compact(const void *X, int64_t row_bytes, const int64_t *hi
 stca_status stca_attention_backward(stca_handle *h, int32_t layer, const void *U, const float *dY,
                                     const int64_t *tgt_off, int64_t B, float *dXt, float *dU, void *stream);
 
+/* Backward of layer `layer`'s history path, Eq.(1)-(2): X~ = LN(SwiGLUFFN(X)) over the
+ * rows the last projection kept (bf16 path).  X: DEVICE bf16 [rows x d], those rows in cache order
+ * (X itself when nothing was truncated; rows must equal the cache's row count).  Given dXt = dLoss/dX~
+ * (DEVICE fp32 [rows x d], e.g. from stca_attention_backward), ACCUMULATES dX += dLoss/dX (DEVICE fp32
+ * [rows x d]; sum over the layers by calling once per layer) and WRITES the layer's weight gradients
+ * dWu, dWv [d x rd], dWo [rd x d], dgamma, dbeta [d] (DEVICE fp32, the weights' [in x out] orientation).
+ * The forward is recomputed (no activations are kept); the GEMMs run on cuBLAS (bf16 operands, fp32
+ * accumulation), SwiGLU and LayerNorm backward on kernels of the library.  Each history row appears once
+ * per request however many targets share it: the gradients are aggregated at the request level.
+ * Asynchronous on `stream`.  STATE without a projection, SHAPE for a row-count mismatch, UNSUPPORTED off
+ * the bf16 path or over a session cache. */
+stca_status stca_history_backward(stca_handle *h, int32_t layer, const void *X, int64_t rows, const float *dXt,
+                                  float *dX, float *dWu, float *dWv, float *dWo, float *dgamma, float *dbeta,
+                                  void *stream);
+
 /* ---- input-encoding prologue ----
  * PAPER.md §3.1.1 "Input encoding" (video, action-type and position embeddings fused into x_j)
  * and the time-delta side information (request time minus item timestamp); additive fusion as

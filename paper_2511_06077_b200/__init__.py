@@ -207,6 +207,22 @@ class STCA:
                                                   ctypes.c_void_p(_stream(stream))))
         return dXt, dU
 
+    def history_backward(self, layer: int, X, dXt, dX=None, stream=None):
+        """stca_history_backward (NEXT-1, partial): accumulates dX (float32 CUDA [rows x d]; zeros if None) and
+        returns (dX, {"Wu", "Wv", "Wo", "ln_g", "ln_b"} weight gradients, float32 CUDA) for layer `layer`."""
+        import torch
+        rows = int(X.shape[0])
+        rd = self.r * self.d
+        if dX is None:
+            dX = torch.zeros((rows, self.d), dtype=torch.float32, device=dXt.device)
+        g = {"Wu": torch.empty((self.d, rd), device=dXt.device), "Wv": torch.empty((self.d, rd), device=dXt.device),
+             "Wo": torch.empty((rd, self.d), device=dXt.device), "ln_g": torch.empty(self.d, device=dXt.device),
+             "ln_b": torch.empty(self.d, device=dXt.device)}
+        self._check(lib().stca_history_backward(self._h, int(layer), _ptr(X), rows, _ptr(dXt), _ptr(dX), _ptr(g["Wu"]),
+                                                _ptr(g["Wv"]), _ptr(g["Wo"]), _ptr(g["ln_g"]), _ptr(g["ln_b"]),
+                                                _stream(stream)))
+        return dX, g
+
     def _cache_rows(self) -> int:
         if getattr(self, "_T2", None) is None:
             raise ValueError("pass dXt (the cache holds sum_b L'_b rows) or call project_history with track=True")

@@ -52,7 +52,7 @@ SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy"
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
            "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact",
            "stca_profile", "stca_profile_read", "stca_session_open", "stca_project_history_session",
-           "stca_encode_history", "stca_attention_backward"]
+           "stca_encode_history", "stca_attention_backward", "stca_history_backward"]
 
 
 def lib():
@@ -117,6 +117,9 @@ def lib():
         L.stca_attention_backward.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, _I64P,
                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.stca_attention_backward.restype = ctypes.c_int32
+        L.stca_history_backward.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64] + \
+            [ctypes.c_void_p] * 8
+        L.stca_history_backward.restype = ctypes.c_int32
         L.stca_session_open.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.stca_session_open.restype = ctypes.c_int32
         L.stca_project_history_session.argtypes = [ctypes.c_void_p, _I64P, _I64P, ctypes.c_void_p, ctypes.c_int64,

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "kernels_cc.cu", "tc_gemm.cu", "tc_host.cu", "tc_proj.cu", "tc_attn.cu", "tc_attn_wide.cu", "tc_attn_narrow.cu", "rlb_batch.cu",
            "encode.cu", "tc_attn_pair.cu", "tc_chain.cu",
-           "tc_attn_bwd.cu"]
+           "tc_attn_bwd.cu", "hist_bwd.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), variant: str =
     with cf.ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose, defines, bdir), SOURCES))
     tmp = out + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas"])
     os.replace(tmp, out)
     return out
 

@@ -128,6 +128,7 @@ struct ProfRegion {
 struct LayerW {
   void *W1h = nullptr, *Woh = nullptr;  // history FFN: [d x 2rd] interleaved (u_j, v_j), [rd x d]
   float *gh = nullptr, *bh = nullptr;
+  void *Wu = nullptr, *Wv = nullptr;    // history FFN Wu, Wv [d x rd] row-major (the backward's GEMMs)
   void *W1q = nullptr, *Woq = nullptr;  // query FFN
   float *gq = nullptr, *bq = nullptr;   // layer 1 only
   void *WQK = nullptr;                  // [d x h d], scaled by log2(e)/sqrt(d_h)
@@ -166,6 +167,8 @@ struct stca_handle {
   int64_t sess_cap = 0, sess_head = 0;
   std::map<int64_t, SessEntry> sess;      // user -> entry
   std::map<int64_t, int64_t> sess_pos;    // cache row offset -> user (ordered, for eviction by overlap)
+  void *blas = nullptr;  // cuBLAS handle of the history-path backward (created on first use)
+  DevBuf bwd_scratch;
   // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
   int cap_layer = 0;
   void *cap_U = nullptr, *cap_Y = nullptr;
@@ -184,7 +187,7 @@ struct stca_handle {
 
 static DevBuf *const *all_bufs(stca_handle *h, int *n) {
   static thread_local DevBuf *v[32];
-  DevBuf *list[] = {&h->xt_cache, &h->xin[0], &h->xin[1], &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
+  DevBuf *list[] = {&h->xt_cache, &h->xin[0], &h->xin[1], &h->bwd_scratch, &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
                     &h->part,     &h->partg, &h->plan,   &h->zout,   &h->Zout};
   *n = (int)(sizeof list / sizeof list[0]);
@@ -580,6 +583,8 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
     LayerW &Ly = h->L[i - 1];
     std::string p = "L" + std::to_string(i) + ".";
     if (!ffn(p + "hist", &Ly.W1h, &Ly.Woh, &Ly.tc)) return bad(fail(h, STCA_ERR_OOM, "upload failed (%s)", p.c_str()));
+    if (!(Ly.Wu = upload(h, W(p + "hist.Wu"), (size_t)d * rd)) || !(Ly.Wv = upload(h, W(p + "hist.Wv"), (size_t)d * rd)))
+      return bad(fail(h, STCA_ERR_OOM, "upload failed (%shist.Wu/Wv)", p.c_str()));
     if (W(p + "qry.Wu") == W(p + "hist.Wu") && W(p + "qry.Wv") == W(p + "hist.Wv") && W(p + "qry.Wo") == W(p + "hist.Wo")) {
       Ly.W1q = Ly.W1h;
       Ly.Woq = Ly.Woh;
@@ -672,6 +677,7 @@ extern "C" void stca_destroy(stca_handle *h) {
   for (int i = 0; i < nb; ++i) bufs[i]->release();
   cudaDeviceSynchronize();  // stream-ordered frees on the legacy stream
   h->stage.release();
+  stca::hist_bwd_release(h->blas);
   for (ProfRegion &r : h->prof_open) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1541,5 +1547,30 @@ extern "C" stca_status stca_attention_backward(stca_handle *h, int32_t layer, co
   if (s != STCA_OK) return s;
   const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)(layer - 1) * h->T2 * d * h->es;
   CU(stca::tc_attention_bwd(U, NQ, Xt, h->T2, h->seg.as<stca::AttnItem>(), (int64_t)items.size(), dY, dXt, dU, st));
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_history_backward(stca_handle *h, int32_t layer, const void *X, int64_t rows,
+                                             const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
+                                             float *dgamma, float *dbeta, void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (h->B < 0) return fail(h, STCA_ERR_STATE, "stca_history_backward before stca_project_history");
+  if (!h->bf16) return fail(h, STCA_ERR_UNSUPPORTED, "the history backward runs on the bf16 path");
+  if (h->sess_on) return fail(h, STCA_ERR_UNSUPPORTED, "no history backward over a session cache");
+  if (layer < 1 || layer > h->cfg.M) return fail(h, STCA_ERR_INVALID_ARG, "layer %d outside 1..%d", layer, h->cfg.M);
+  if (rows != h->T2)
+    return fail(h, STCA_ERR_SHAPE, "X has %lld rows, the projection kept %lld", (long long)rows, (long long)h->T2);
+  if (rows > 0 && (!X || !dXt || !dX)) return fail(h, STCA_ERR_INVALID_ARG, "NULL X / dXt / dX");
+  if (!dWu || !dWv || !dWo || !dgamma || !dbeta) return fail(h, STCA_ERR_INVALID_ARG, "NULL weight gradient");
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = h->cfg.d, rd = h->cfg.r * d;
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
+  CU(h->bwd_scratch.ensure(stca::hist_bwd_scratch_bytes(d, rd, R), st));
+  LayerW &Ly = h->L[layer - 1];
+  CU(stca::hist_bwd(&h->blas, (const bf16 *)X, rows, d, rd, (const bf16 *)Ly.Wu, (const bf16 *)Ly.Wv,
+                    (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, dX, dWu, dWv, dWo, dgamma, dbeta,
+                    h->bwd_scratch.p, R, st));
   return STCA_OK;
 }

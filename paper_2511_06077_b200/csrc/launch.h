@@ -59,6 +59,13 @@ cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items
                            const float *part,
                            int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st);
 
+// ---- history-path backward (hist_bwd.cu; NEXT-1 partial) ----
+size_t hist_bwd_scratch_bytes(int d, int rd, int64_t R);
+cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, const bf16 *Wu, const bf16 *Wv,
+                     const bf16 *Wo, const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv,
+                     float *dWo, float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st);
+void hist_bwd_release(void *blas);
+
 // ---- utility kernels ----
 cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg /*[n][3]: src,dst,len*/, int64_t nseg,
                         int64_t max_len, int row_bytes, cudaStream_t st);

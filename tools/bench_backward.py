@@ -65,6 +65,26 @@ def main():
     bound = "tensor" if flops / byts >= ridge else "hbm"
     ach = flops / (ms * 1e-3) / 1e12 if bound == "tensor" else byts / (ms * 1e-3) / 1e9
     peak = pk["bf16_tflops"] if bound == "tensor" else pk["hbm_gbs"]
+    # the history-path backward of the same layer (stca_history_backward): 18 r d^2 FLOPs per kept row
+    # (recompute 6 r d^2 + dWo, dH, dWu, dWv, dX 12 r d^2), tensor-bound
+    Xk = X if not c.L_infer else None
+    hist = None
+    if Xk is not None and int(Xk.shape[0]) == T2:
+        dXh = torch.zeros(T2, c.d, device="cuda")
+        for _ in range(2):
+            m.history_backward(1, Xk, dX, dX=dXh, stream=st)
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(st)
+        for _ in range(3):
+            m.history_backward(1, Xk, dX, dX=dXh, stream=st)
+        h1.record(st)
+        torch.cuda.synchronize()
+        hms = h0.elapsed_time(h1) / 3
+        hfl = 18.0 * c.r * c.d * c.d * T2
+        hist = {"kernel": "history-path backward (stca_history_backward, one layer; cuBLAS GEMMs + kernels)",
+                "ms_per_call": hms, "achieved_TFLOPs": hfl / (hms * 1e-3) / 1e12,
+                "frac_of_bf16_peak": hfl / (hms * 1e-3) / 1e12 / pk["bf16_tflops"], "algorithmic_flops": hfl}
     print(json.dumps({"kernel": "attention backward (stca_attention_backward, one layer)", "config": a.config,
                       "ms_per_launch": ms, "targets_per_s": wl.Nt / (ms * 1e-3),
                       "roofline": {"bound": bound, "achieved": ach, "peak": peak,
@@ -72,7 +92,7 @@ def main():
                                    "algorithmic_flops": flops, "algorithmic_bytes": byts,
                                    "note": "the kernel reads X~ twice (pass 1: softmax statistics; pass 2: "
                                            "gradients): algorithmic bytes count it once"},
-                      "T": T2, "N_t": wl.Nt}), flush=True)
+                      "T": T2, "N_t": wl.Nt, "history_backward": hist}), flush=True)
     m.close()
 
 
