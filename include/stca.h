@@ -288,6 +288,35 @@ stca_status stca_history_backward(stca_handle *h, int32_t layer, const void *X, 
                                   float *dX, float *dWu, float *dWv, float *dWo, float *dgamma, float *dbeta,
                                   void *stream);
 
+/* ---- backward of the WHOLE stack ----
+ * PAPER.md Eq.(14) trains the stack of Eq.(2)-(9) end to end; under RLB the gradients of a
+ * request's shared history are aggregated over its targets inside the request.  For the
+ * last projection (bf16 path, d = 128, no split-history, no session cache): runs the forward over x_t
+ * (DEVICE bf16 [N_t x d], as stca_forward; Z_H into out_Z, DEVICE fp32 [N_t x M x d], or internal scratch
+ * when NULL) keeping every layer's U and Y, then the vector-Jacobian product of
+ *     loss = sum(dZ * Z_H) + sum(dz * z)      (dZ DEVICE fp32 [N_t x M x d]; dz DEVICE fp32 [N_t x d] or NULL)
+ * and WRITES
+ *   - for every stca_grad {name, grad} given: d loss / d weight role `name` (the names and [rows x cols]
+ *     of stca_create's weights; DEVICE fp32, same orientation).  Gradients are per ROLE: where one
+ *     parameter serves several roles (the shared-FFN reading passes a layer's history FFN as its query
+ *     FFN), its gradient is the sum of its roles'.  Roles not listed are computed into scratch.
+ *   - dX (DEVICE fp32 [rows x d] or NULL): d loss / d X over the rows the projection kept, in cache order
+ *     (X: DEVICE bf16, those rows, as stca_history_backward; rows must equal the cache's row count);
+ *   - dxt (DEVICE fp32 [N_t x d] or NULL): d loss / d x_t.
+ * Per layer, from the last: target-side GEMMs of Eq.(6)-(7) in fp32 (cuBLAS), the attention backward
+ * (tcgen05 kernel, dX~ summed over the request's target-head rows inside the MMA), the history path's
+ * LN + SwiGLU-FFN backward (stca_history_backward's kernels).  Asynchronous on `stream`.  STATE without a
+ * projection or for a B mismatch; UNSUPPORTED off the bf16 d = 128 path, in split-history mode or over a
+ * session cache; SHAPE for a row-count mismatch; INVALID_ARG for an unknown / duplicate gradient name,
+ * NULL or host buffers.  Nothing is enqueued on an error found before the first launch. */
+typedef struct {
+  const char *name; /* a weight role of stca_create, e.g. "L2.WC", "L1.hist.ln_g", "z.Wo" */
+  float *grad;      /* DEVICE fp32, rows x cols of that role */
+} stca_grad;
+stca_status stca_backward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                          const void *X, int64_t rows, const float *dZ, const float *dz, const stca_grad *grads,
+                          int32_t n_grads, float *dX, float *dxt, float *out_Z, void *stream);
+
 /* ---- input-encoding prologue ----
  * PAPER.md §3.1.1 "Input encoding" (video, action-type and position embeddings fused into x_j)
  * and the time-delta side information (request time minus item timestamp); additive fusion as

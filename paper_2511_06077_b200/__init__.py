@@ -20,7 +20,7 @@ import numpy as np
 
 from ._lib import (STCA_BF16, STCA_FP32, StcaError, lib, plan_attention, plan_chunks, plan_persistent, plan_shards,  # noqa: F401,E501
                    plan_split, plan_suffix, status_string, validate_offsets, kernel_launches, EXCHANGE_FN, ALLOC_FN,
-                   FREE_FN, PHASES, _Config, _Tensor, _EmbedTables, LIB_PATH)
+                   FREE_FN, PHASES, _Config, _Tensor, _EmbedTables, _Grad, LIB_PATH)
 
 __all__ = ["STCA", "StcaError", "plan_attention", "plan_chunks", "plan_persistent", "plan_shards", "plan_split", "plan_suffix",
            "validate_offsets", "status_string", "LIB_PATH", "nccl_exchange", "ThreadExchange", "rlb_allocate",
@@ -123,6 +123,7 @@ class STCA:
             raise ValueError(f"allocator must be 'torch' or 'cuda', not {allocator!r}")
         # weights: host float32; identical array objects keep identical pointers (reading R5 aliasing)
         conv, keep = {}, []
+        self._shapes = {}
         tens = (_Tensor * len(weights))()
         for i, (name, arr) in enumerate(weights.items()):
             key = id(arr)
@@ -133,6 +134,7 @@ class STCA:
             bname = name.encode()
             keep.append(bname)
             rows, cols = (1, a.size) if a.ndim == 1 else a.shape
+            self._shapes[name] = (rows, cols)
             tens[i].name = bname
             tens[i].data = a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
             tens[i].rows, tens[i].cols = rows, cols
@@ -222,6 +224,31 @@ class STCA:
                                                 _ptr(g["Wv"]), _ptr(g["Wo"]), _ptr(g["ln_g"]), _ptr(g["ln_b"]),
                                                 _stream(stream)))
         return dX, g
+
+    def backward(self, xt, tgt_off, X, dZ, dz=None, grads=None, dX=None, dxt=None, out_Z=None, stream=None):
+        """stca_backward (NEXT-1): forward over x_t, then d(sum(dZ Z_H) + sum(dz z)) for every weight role in
+        `grads` (name -> float32 CUDA tensor shaped like the weight; None: all roles, allocated here), the kept
+        history rows X (dX) and x_t (dxt).  Returns (grads, dX, dxt)."""
+        import torch
+        off = _i64(tgt_off)
+        B = off.shape[0] - 1
+        Nt, rows = int(xt.shape[0]), int(X.shape[0])
+        dev = dZ.device
+        if grads is None:
+            grads = {n: torch.empty(tuple(sh), dtype=torch.float32, device=dev) for n, sh in self._shapes.items()}
+        if dX is None:
+            dX = torch.empty((rows, self.d), dtype=torch.float32, device=dev)
+        if dxt is None:
+            dxt = torch.empty((Nt, self.d), dtype=torch.float32, device=dev)
+        keep = [n.encode() for n in grads]
+        arr = (_Grad * max(len(grads), 1))()
+        for i, (n, t) in enumerate(grads.items()):
+            arr[i] = _Grad(keep[i], _ptr(t))
+        self._check(lib().stca_backward(self._h, _ptr(xt), Nt, off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), B,
+                                        _ptr(X), rows, _ptr(dZ), _ptr(dz) if dz is not None else None, arr,
+                                        len(grads), _ptr(dX), _ptr(dxt), _ptr(out_Z) if out_Z is not None else None,
+                                        _stream(stream)))
+        return grads, dX, dxt
 
     def _cache_rows(self) -> int:
         if getattr(self, "_T2", None) is None:

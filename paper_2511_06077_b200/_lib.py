@@ -32,6 +32,10 @@ class _Tensor(ctypes.Structure):
                 ("cols", ctypes.c_int64)]
 
 
+class _Grad(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("grad", ctypes.c_void_p)]
+
+
 class _EmbedTables(ctypes.Structure):
     _fields_ = [("video", ctypes.c_void_p), ("n_video", ctypes.c_int64), ("action", ctypes.c_void_p),
                 ("n_action", ctypes.c_int64), ("position", ctypes.c_void_p), ("n_position", ctypes.c_int64),
@@ -52,7 +56,7 @@ SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy"
            "stca_plan_chunks", "stca_plan_attention", "stca_plan_shards", "stca_kernel_launches",
            "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact",
            "stca_profile", "stca_profile_read", "stca_session_open", "stca_project_history_session",
-           "stca_encode_history", "stca_attention_backward", "stca_history_backward"]
+           "stca_encode_history", "stca_attention_backward", "stca_history_backward", "stca_backward"]
 
 
 def lib():
@@ -120,6 +124,11 @@ def lib():
         L.stca_history_backward.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64] + \
             [ctypes.c_void_p] * 8
         L.stca_history_backward.restype = ctypes.c_int32
+        L.stca_backward.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _I64P, ctypes.c_int64,
+                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.POINTER(_Grad), ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p]
+        L.stca_backward.restype = ctypes.c_int32
         L.stca_session_open.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.stca_session_open.restype = ctypes.c_int32
         L.stca_project_history_session.argtypes = [ctypes.c_void_p, _I64P, _I64P, ctypes.c_void_p, ctypes.c_int64,

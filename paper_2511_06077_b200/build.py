@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "kernels_cc.cu", "tc_gemm.cu", "tc_host.cu", "tc_proj.cu", "tc_attn.cu", "tc_attn_wide.cu", "tc_attn_narrow.cu", "rlb_batch.cu",
            "encode.cu", "tc_attn_pair.cu", "tc_chain.cu",
-           "tc_attn_bwd.cu", "hist_bwd.cu"]
+           "tc_attn_bwd.cu", "hist_bwd.cu", "stack_bwd.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]

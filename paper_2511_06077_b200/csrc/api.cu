@@ -167,8 +167,13 @@ struct stca_handle {
   int64_t sess_cap = 0, sess_head = 0;
   std::map<int64_t, SessEntry> sess;      // user -> entry
   std::map<int64_t, int64_t> sess_pos;    // cache row offset -> user (ordered, for eviction by overlap)
-  void *blas = nullptr;  // cuBLAS handle of the history-path backward (created on first use)
+  void *blas = nullptr;  // cuBLAS handle of the backward (created on first use)
   DevBuf bwd_scratch;
+  // stca_backward: fp32 copies of the target-side weights (user orientation; bf16 path, d = 128 only),
+  // the forward's per-layer U and Y (save_act), the target-side scratch, dX~ of one layer, unrequested gradients
+  std::map<std::string, float *> w32;
+  bool save_act = false;
+  DevBuf act, sbwd_scratch, dxt_buf, gsink, dxsink;
   // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
   int cap_layer = 0;
   void *cap_U = nullptr, *cap_Y = nullptr;
@@ -187,7 +192,8 @@ struct stca_handle {
 
 static DevBuf *const *all_bufs(stca_handle *h, int *n) {
   static thread_local DevBuf *v[32];
-  DevBuf *list[] = {&h->xt_cache, &h->xin[0], &h->xin[1], &h->bwd_scratch, &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
+  DevBuf *list[] = {&h->act, &h->sbwd_scratch, &h->dxt_buf, &h->gsink, &h->dxsink,
+                    &h->xt_cache, &h->xin[0], &h->xin[1], &h->bwd_scratch, &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
                     &h->part,     &h->partg, &h->plan,   &h->zout,   &h->Zout};
   *n = (int)(sizeof list / sizeof list[0]);
@@ -454,6 +460,40 @@ static void *upload(stca_handle *h, const float *src, size_t n, bool as_f32 = fa
   return p;
 }
 
+// The weight roles of include/stca.h (names and [rows x cols]), in the order stca_create documents.
+struct Need {
+  std::string name;
+  int64_t rows, cols;
+};
+static std::vector<Need> weight_roles(int d, int r, int M, bool with_z) {
+  const int rd = r * d;
+  std::vector<Need> need;
+  for (int i = 1; i <= M; ++i) {
+    std::string p = "L" + std::to_string(i) + ".";
+    need.push_back({p + "hist.Wu", d, rd});
+    need.push_back({p + "hist.Wv", d, rd});
+    need.push_back({p + "hist.Wo", rd, d});
+    need.push_back({p + "hist.ln_g", 1, d});
+    need.push_back({p + "hist.ln_b", 1, d});
+    need.push_back({p + "qry.Wu", d, rd});
+    need.push_back({p + "qry.Wv", d, rd});
+    need.push_back({p + "qry.Wo", rd, d});
+    if (i == 1) {
+      need.push_back({"L1.qry.ln_g", 1, d});
+      need.push_back({"L1.qry.ln_b", 1, d});
+    }
+    for (const char *k : {"WQ", "WK", "WV", "WO"}) need.push_back({p + k, d, d});
+    if (i >= 2) need.push_back({p + "WC", (int64_t)i * d, d});
+  }
+  if (with_z) {
+    need.push_back({"z.WZ", (int64_t)(M + 1) * d, d});
+    need.push_back({"z.Wu", d, rd});
+    need.push_back({"z.Wv", d, rd});
+    need.push_back({"z.Wo", rd, d});
+  }
+  return need;
+}
+
 extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w, int32_t n_w, stca_handle **out) {
   if (!cfg || !out || (n_w > 0 && !w)) return STCA_ERR_INVALID_ARG;
   *out = nullptr;
@@ -512,34 +552,7 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
     byname[w[i].name] = &w[i];
   }
   const int rd = r * d;
-  struct Need {
-    std::string name;
-    int64_t rows, cols;
-  };
-  std::vector<Need> need;
-  for (int i = 1; i <= M; ++i) {
-    std::string p = "L" + std::to_string(i) + ".";
-    need.push_back({p + "hist.Wu", d, rd});
-    need.push_back({p + "hist.Wv", d, rd});
-    need.push_back({p + "hist.Wo", rd, d});
-    need.push_back({p + "hist.ln_g", 1, d});
-    need.push_back({p + "hist.ln_b", 1, d});
-    need.push_back({p + "qry.Wu", d, rd});
-    need.push_back({p + "qry.Wv", d, rd});
-    need.push_back({p + "qry.Wo", rd, d});
-    if (i == 1) {
-      need.push_back({"L1.qry.ln_g", 1, d});
-      need.push_back({"L1.qry.ln_b", 1, d});
-    }
-    for (const char *k : {"WQ", "WK", "WV", "WO"}) need.push_back({p + k, d, d});
-    if (i >= 2) need.push_back({p + "WC", (int64_t)i * d, d});
-  }
-  if (cfg->with_z) {
-    need.push_back({"z.WZ", (int64_t)(M + 1) * d, d});
-    need.push_back({"z.Wu", d, rd});
-    need.push_back({"z.Wv", d, rd});
-    need.push_back({"z.Wo", rd, d});
-  }
+  const std::vector<Need> need = weight_roles(d, r, M, cfg->with_z != 0);
   for (const Need &n : need) {
     auto it = byname.find(n.name);
     if (it == byname.end()) return bad(fail(h, STCA_ERR_SHAPE, "missing weight '%s' (%lld x %lld)", n.name.c_str(),
@@ -661,6 +674,14 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
     if (!h->WZ) return bad(fail(h, STCA_ERR_OOM, "alloc failed"));
     if (h->bf16 && !stca::tc_prepare_layer(nullptr, nullptr, h->WZ, M + 1, d, hh, &h->tcz, [&](size_t n) { return dalloc(h, n); }))
       return bad(fail(h, STCA_ERR_OOM, "tc repack failed"));
+  }
+  if (h->bf16 && d == 128) {  // the whole-stack backward (stca_backward) works on fp32 target-side weights
+    for (const Need &n : need) {
+      if (n.name.find(".hist.") != std::string::npos) continue;
+      float *p = (float *)upload(h, W(n.name), (size_t)(n.rows * n.cols), true);
+      if (!p) return bad(fail(h, STCA_ERR_OOM, "upload failed (%s)", n.name.c_str()));
+      h->w32[n.name] = p;
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bad(fail(h, STCA_ERR_CUDA, "create: device error"));
   *out = h;
@@ -1393,6 +1414,9 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     if (h->cap_layer == i) {  // stage-isolated test hook: this layer's U (a3 output) and Y (a4 output)
       CU(cudaMemcpyAsync(h->cap_U, h->U.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
     }
+    if (h->save_act)  // stca_backward: U of layer i (slot 2 (i - 1))
+      CU(cudaMemcpyAsync(h->act.as<uint8_t>() + (size_t)2 * (i - 1) * NQ * d * es, h->U.p, (size_t)NQ * d * es,
+                         cudaMemcpyDeviceToDevice, st));
     pa = prof_begin(h, st);
     CU(stca::merge_partials(h->bf16, d_mitems, (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
                             G, (int64_t)part_bytes, h->Y.p, st));
@@ -1402,6 +1426,9 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       CU(cudaMemcpyAsync(h->cap_Y, h->Y.p, (size_t)NQ * d * es, cudaMemcpyDeviceToDevice, st));
       h->cap_layer = 0;
     }
+    if (h->save_act)  // ... and its attention output Y (slot 2 (i - 1) + 1)
+      CU(cudaMemcpyAsync(h->act.as<uint8_t>() + (size_t)(2 * (i - 1) + 1) * NQ * d * es, h->Y.p, (size_t)NQ * d * es,
+                         cudaMemcpyDeviceToDevice, st));
     if (chain) {  // a5 (+ a6, a3 of layer i + 1; or a7 after the last layer) as one kernel
       stca::TcChain c = chain_base(i < M ? 1 : 2);
       c.Y = h->Y.p;
@@ -1502,6 +1529,27 @@ extern "C" stca_status stca_debug_capture(stca_handle *h, int32_t layer, void *U
 // ===========================================================================
 // NEXT-1 (partial): backward of one layer's attention with request-level gradient aggregation
 // ===========================================================================
+// attention-backward work items: (request, block of <= 64 query rows) over ALL of the request's kept keys
+static std::vector<stca::AttnItem> bwd_items(const stca_handle *h, const int64_t *tgt_off, int64_t B) {
+  const int hh = h->cfg.h;
+  std::vector<stca::AttnItem> items;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
+    const int64_t nqb = (rows + 63) / 64;
+    for (int64_t qb = 0; qb < nqb; ++qb) {
+      stca::AttnItem a{};
+      a.qrow0 = tgt_off[b] * hh + 64 * qb;
+      a.nq = (int32_t)std::min<int64_t>(64, rows - 64 * qb);
+      a.key0 = h->coff[b];
+      a.klen = (int32_t)h->len[b];
+      a.chunk = 0;
+      a.part_row = nqb > 1 ? 1 : 0;  // several items add into the request's dX~ rows
+      items.push_back(a);
+    }
+  }
+  return items;
+}
+
 extern "C" stca_status stca_attention_backward(stca_handle *h, int32_t layer, const void *U, const float *dY,
                                                const int64_t *tgt_off, int64_t B, float *dXt, float *dU,
                                                void *stream) {
@@ -1524,22 +1572,7 @@ extern "C" stca_status stca_attention_backward(stca_handle *h, int32_t layer, co
   cudaStream_t st = (cudaStream_t)stream;
   const int d = h->cfg.d, hh = h->cfg.h;
   const int64_t NQ = Nt * hh;
-  // work items: (request, block of <= 64 query rows) over ALL of the request's kept keys
-  std::vector<stca::AttnItem> items;
-  for (int64_t b = 0; b < B; ++b) {
-    const int64_t rows = (tgt_off[b + 1] - tgt_off[b]) * hh;
-    const int64_t nqb = (rows + 63) / 64;
-    for (int64_t qb = 0; qb < nqb; ++qb) {
-      stca::AttnItem a{};
-      a.qrow0 = tgt_off[b] * hh + 64 * qb;
-      a.nq = (int32_t)std::min<int64_t>(64, rows - 64 * qb);
-      a.key0 = h->coff[b];
-      a.klen = (int32_t)h->len[b];
-      a.chunk = 0;
-      a.part_row = nqb > 1 ? 1 : 0;  // several items add into the request's dX~ rows
-      items.push_back(a);
-    }
-  }
+  std::vector<stca::AttnItem> items = bwd_items(h, tgt_off, B);
   // dX~ rows of requests without targets (and the sums of multi-block requests) start from zero
   CU(cudaMemsetAsync(dXt, 0, (size_t)h->T2 * d * sizeof(float), st));
   if (items.empty()) return STCA_OK;
@@ -1572,5 +1605,198 @@ extern "C" stca_status stca_history_backward(stca_handle *h, int32_t layer, cons
   CU(stca::hist_bwd(&h->blas, (const bf16 *)X, rows, d, rd, (const bf16 *)Ly.Wu, (const bf16 *)Ly.Wv,
                     (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, dX, dWu, dWv, dWo, dgamma, dbeta,
                     h->bwd_scratch.p, R, st));
+  return STCA_OK;
+}
+
+// ===========================================================================
+// NEXT-1: backward of the whole stack (forward with saved U / Y, then target side in reverse order with
+// each layer's attention and history backward in between)
+// ===========================================================================
+namespace {
+struct BwdCtx {
+  stca_handle *h;
+  const void *X;
+  int64_t rows, NQ, nit;
+  const stca::AttnItem *items;
+  float *dX;
+  float *gWu[STCA_MAX_LAYERS], *gWv[STCA_MAX_LAYERS], *gWo[STCA_MAX_LAYERS], *gg[STCA_MAX_LAYERS], *gb[STCA_MAX_LAYERS];
+  cudaStream_t st;
+};
+}  // namespace
+
+static cudaError_t bwd_attn_hist(void *ctx, int layer, const float *dY, float *dU) {
+  BwdCtx &c = *(BwdCtx *)ctx;
+  stca_handle *h = c.h;
+  const int d = h->cfg.d, rd = h->cfg.r * d, L = layer - 1;
+  float *dXt = h->dxt_buf.as<float>();
+  cudaError_t e = cudaMemsetAsync(dXt, 0, (size_t)h->T2 * d * 4, c.st);
+  if (e != cudaSuccess) return e;
+  const void *U = h->act.as<uint8_t>() + (size_t)2 * L * c.NQ * d * h->es;
+  const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)L * h->T2 * d * h->es;
+  if (c.nit > 0 && (e = stca::tc_attention_bwd(U, c.NQ, Xt, h->T2, c.items, c.nit, dY, dXt, dU, c.st)) != cudaSuccess)
+    return e;
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(c.rows, 1), 1 << 16);
+  LayerW &Ly = h->L[L];
+  return stca::hist_bwd(&h->blas, (const bf16 *)c.X, c.rows, d, rd, (const bf16 *)Ly.Wu, (const bf16 *)Ly.Wv,
+                        (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, c.dX, c.gWu[L], c.gWv[L], c.gWo[L], c.gg[L],
+                        c.gb[L], h->bwd_scratch.p, R, c.st);
+}
+
+extern "C" stca_status stca_backward(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
+                                     const void *X, int64_t rows, const float *dZ, const float *dz,
+                                     const stca_grad *grads, int32_t n_grads, float *dX, float *dxt, float *out_Z,
+                                     void *stream) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (h->sticky) return fail(h, STCA_ERR_CUDA, "handle is in a sticky CUDA error state: %s", h->err.c_str());
+  if (h->B < 0) return fail(h, STCA_ERR_STATE, "stca_backward before stca_project_history");
+  if (B != h->B) return fail(h, STCA_ERR_STATE, "B=%lld differs from the projected B=%lld", (long long)B, (long long)h->B);
+  if (!h->bf16 || h->cfg.d != 128)
+    return fail(h, STCA_ERR_UNSUPPORTED, "the backward runs on the bf16 path with d = 128 (d=%d)", h->cfg.d);
+  if (h->cfg.split_world > 1) return fail(h, STCA_ERR_UNSUPPORTED, "no backward in split-history mode");
+  if (h->sess_on) return fail(h, STCA_ERR_UNSUPPORTED, "no backward over a session cache");
+  if (!tgt_off) return fail(h, STCA_ERR_INVALID_ARG, "tgt_off is NULL");
+  int64_t badi = -1;
+  stca_status s = check_offsets(tgt_off, B, Nt, false, &badi);
+  if (s != STCA_OK) return fail(h, s, "tgt_off invalid at request %lld", (long long)badi);
+  if (rows != h->T2)
+    return fail(h, STCA_ERR_SHAPE, "X has %lld rows, the projection kept %lld", (long long)rows, (long long)h->T2);
+  if (n_grads < 0 || (n_grads > 0 && !grads)) return fail(h, STCA_ERR_INVALID_ARG, "bad gradient list");
+  const int d = h->cfg.d, hh = h->cfg.h, r = h->cfg.r, M = h->cfg.M, rd = r * d;
+  const bool wz = h->cfg.with_z != 0;
+  // every device argument must be device memory (the backward keeps no host staging)
+  auto dev = [&](const void *p, const char *what) -> stca_status {
+    if (p && !is_device_ptr(p)) return fail(h, STCA_ERR_INVALID_ARG, "%s must be device memory", what);
+    return STCA_OK;
+  };
+  if (Nt > 0 && (!xt || !dZ)) return fail(h, STCA_ERR_INVALID_ARG, "NULL x_t / dZ");
+  if (rows > 0 && !X) return fail(h, STCA_ERR_INVALID_ARG, "NULL X");
+  if (dz && !wz) return fail(h, STCA_ERR_INVALID_ARG, "dz given but the handle has with_z = 0");
+  for (auto pr : {std::make_pair((const void *)xt, "x_t"), std::make_pair((const void *)X, "X"),
+                  std::make_pair((const void *)dZ, "dZ"), std::make_pair((const void *)dz, "dz"),
+                  std::make_pair((const void *)dX, "dX"), std::make_pair((const void *)dxt, "dxt"),
+                  std::make_pair((const void *)out_Z, "out_Z")})
+    if ((s = dev(pr.first, pr.second)) != STCA_OK) return s;
+  // gradient buffers by role name; roles not asked for accumulate into a sink
+  const std::vector<Need> roles = weight_roles(d, r, M, wz);
+  std::map<std::string, float *> g;
+  for (int32_t i = 0; i < n_grads; ++i) {
+    if (!grads[i].name || !grads[i].grad) return fail(h, STCA_ERR_INVALID_ARG, "gradient %d has a NULL name or buffer", i);
+    bool known = false;
+    for (const Need &n : roles) known |= n.name == grads[i].name;
+    if (!known) return fail(h, STCA_ERR_INVALID_ARG, "unknown weight '%s'", grads[i].name);
+    if (g.count(grads[i].name)) return fail(h, STCA_ERR_INVALID_ARG, "duplicate gradient '%s'", grads[i].name);
+    if ((s = dev(grads[i].grad, grads[i].name)) != STCA_OK) return s;
+    g[grads[i].name] = grads[i].grad;
+  }
+  CU(cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t NQ = Nt * hh;
+  size_t sink = 0;
+  for (const Need &n : roles)
+    if (!g.count(n.name)) sink += (size_t)(n.rows * n.cols + 63) / 64 * 64;
+  CU(h->gsink.ensure(std::max<size_t>(sink, 1) * 4, st));
+  {
+    float *q = h->gsink.as<float>();
+    for (const Need &n : roles)
+      if (!g.count(n.name)) {
+        g[n.name] = q;
+        q += (size_t)(n.rows * n.cols + 63) / 64 * 64;
+      }
+  }
+  for (const Need &n : roles) CU(cudaMemsetAsync(g[n.name], 0, (size_t)n.rows * n.cols * 4, st));
+  if (dX && rows > 0) CU(cudaMemsetAsync(dX, 0, (size_t)rows * d * 4, st));
+  if (Nt == 0) return STCA_OK;  // no target: every gradient is zero
+  // ---- forward, keeping every layer's U and Y ----
+  CU(h->act.ensure((size_t)2 * M * NQ * d * h->es, st));
+  float *Zd = out_Z;
+  if (!Zd) {
+    CU(h->Zout.ensure((size_t)Nt * M * d * 4, st));
+    Zd = h->Zout.as<float>();
+  }
+  h->save_act = true;
+  s = forward_body(h, xt, Nt, tgt_off, B, Zd, nullptr, st);
+  h->save_act = false;
+  if (s != STCA_OK) return s;
+  // ---- backward ----
+  std::vector<stca::AttnItem> items = bwd_items(h, tgt_off, B);
+  if (!items.empty()) {
+    s = upload_plan(h, items.data(), items.size() * sizeof(stca::AttnItem), h->seg, st);
+    if (s != STCA_OK) return s;
+  }
+  CU(h->dxt_buf.ensure((size_t)std::max<int64_t>(h->T2, 1) * d * 4, st));
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
+  CU(h->bwd_scratch.ensure(stca::hist_bwd_scratch_bytes(d, rd, R), st));
+  CU(h->sbwd_scratch.ensure(stca::stack_bwd_scratch_bytes(d, hh, rd, M, Nt), st));
+  // dX: the history backward accumulates into it; without a caller buffer it goes to scratch
+  float *dXd = dX;
+  if (!dXd) {
+    CU(h->dxsink.ensure((size_t)std::max<int64_t>(rows, 1) * d * 4, st));
+    dXd = h->dxsink.as<float>();
+  }
+  BwdCtx c{};
+  c.h = h;
+  c.X = X;
+  c.rows = rows;
+  c.NQ = NQ;
+  c.nit = (int64_t)items.size();
+  c.items = h->seg.as<stca::AttnItem>();
+  c.dX = dXd;
+  c.st = st;
+  stca::StackBwd a{};
+  a.d = d;
+  a.h = hh;
+  a.rd = rd;
+  a.M = M;
+  a.eps = h->cfg.ln_eps;
+  a.with_z = wz;
+  a.Nt = Nt;
+  a.xt = (const bf16 *)xt;
+  a.dZ = dZ;
+  a.dz = dz;
+  for (int i = 1; i <= M; ++i) {
+    const std::string p = "L" + std::to_string(i) + ".";
+    const int L = i - 1;
+    a.Y[L] = (const bf16 *)(h->act.as<uint8_t>() + (size_t)(2 * L + 1) * NQ * d * h->es);
+    a.qWu[L] = h->w32[p + "qry.Wu"];
+    a.qWv[L] = h->w32[p + "qry.Wv"];
+    a.qWo[L] = h->w32[p + "qry.Wo"];
+    a.WQ[L] = h->w32[p + "WQ"];
+    a.WK[L] = h->w32[p + "WK"];
+    a.WV[L] = h->w32[p + "WV"];
+    a.WO[L] = h->w32[p + "WO"];
+    a.WC[L] = i >= 2 ? h->w32[p + "WC"] : nullptr;
+    a.g_qWu[L] = g[p + "qry.Wu"];
+    a.g_qWv[L] = g[p + "qry.Wv"];
+    a.g_qWo[L] = g[p + "qry.Wo"];
+    a.g_WQ[L] = g[p + "WQ"];
+    a.g_WK[L] = g[p + "WK"];
+    a.g_WV[L] = g[p + "WV"];
+    a.g_WO[L] = g[p + "WO"];
+    a.g_WC[L] = i >= 2 ? g[p + "WC"] : nullptr;
+    c.gWu[L] = g[p + "hist.Wu"];
+    c.gWv[L] = g[p + "hist.Wv"];
+    c.gWo[L] = g[p + "hist.Wo"];
+    c.gg[L] = g[p + "hist.ln_g"];
+    c.gb[L] = g[p + "hist.ln_b"];
+  }
+  a.qg = h->w32["L1.qry.ln_g"];
+  a.qb = h->w32["L1.qry.ln_b"];
+  a.g_qg = g["L1.qry.ln_g"];
+  a.g_qb = g["L1.qry.ln_b"];
+  if (wz) {
+    a.WZ = h->w32["z.WZ"];
+    a.zWu = h->w32["z.Wu"];
+    a.zWv = h->w32["z.Wv"];
+    a.zWo = h->w32["z.Wo"];
+    a.g_WZ = g["z.WZ"];
+    a.g_zWu = g["z.Wu"];
+    a.g_zWv = g["z.Wv"];
+    a.g_zWo = g["z.Wo"];
+  }
+  a.dxt = dxt;
+  a.attn_hist = bwd_attn_hist;
+  a.ctx = &c;
+  a.scratch = h->sbwd_scratch.p;
+  CU(stca::stack_bwd(&h->blas, a, st));
   return STCA_OK;
 }

@@ -6,6 +6,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "stca.h"
 
 namespace stca {
 
@@ -65,6 +66,32 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
                      const bf16 *Wo, const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv,
                      float *dWo, float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st);
 void hist_bwd_release(void *blas);
+
+// ---- target-side backward of the whole stack (stack_bwd.cu; NEXT-1) ----
+// Weights fp32 in the user's [in x out] orientation; g_* gradients fp32, ACCUMULATED (zero them first).
+// Per layer index L = i - 1; WC[0] / g_WC[0] unused.
+struct StackBwd {
+  int d, h, rd, M;
+  float eps;
+  bool with_z;
+  int64_t Nt;
+  const bf16 *xt;                        // [Nt x d]
+  const bf16 *Y[STCA_MAX_LAYERS];        // the forward's attention outputs [Nt h x d]
+  const float *dZ, *dz;                  // [Nt x M x d], [Nt x d] or NULL
+  const float *qWu[STCA_MAX_LAYERS], *qWv[STCA_MAX_LAYERS], *qWo[STCA_MAX_LAYERS], *qg, *qb;
+  const float *WQ[STCA_MAX_LAYERS], *WK[STCA_MAX_LAYERS], *WV[STCA_MAX_LAYERS], *WO[STCA_MAX_LAYERS];
+  const float *WC[STCA_MAX_LAYERS], *WZ, *zWu, *zWv, *zWo;
+  float *g_qWu[STCA_MAX_LAYERS], *g_qWv[STCA_MAX_LAYERS], *g_qWo[STCA_MAX_LAYERS], *g_qg, *g_qb;
+  float *g_WQ[STCA_MAX_LAYERS], *g_WK[STCA_MAX_LAYERS], *g_WV[STCA_MAX_LAYERS], *g_WO[STCA_MAX_LAYERS];
+  float *g_WC[STCA_MAX_LAYERS], *g_WZ, *g_zWu, *g_zWv, *g_zWo;
+  float *dxt;                            // [Nt x d] written, or NULL
+  // layer i's history side: dY [Nt h x d] -> dU [Nt h x d] (and that layer's dX / history-weight gradients)
+  cudaError_t (*attn_hist)(void *ctx, int layer, const float *dY, float *dU);
+  void *ctx;
+  void *scratch;                         // stack_bwd_scratch_bytes
+};
+size_t stack_bwd_scratch_bytes(int d, int h, int rd, int M, int64_t Nt);
+cudaError_t stack_bwd(void **blas, const StackBwd &a, cudaStream_t st);
 
 // ---- utility kernels ----
 cudaError_t gather_rows(const void *src, void *dst, const int64_t *seg /*[n][3]: src,dst,len*/, int64_t nseg,
