@@ -14,7 +14,8 @@ global request set (seed), partitions it with the library's LPT planner
 (stca_plan_shards over the cost c_b = L'_b 6rd^2M + m_b L'_b 4hdM + m_b c_tgt) and
 runs its own requests; there is no collective on the data path.  value = the global
 N_t / the max over ranks of the device time of a step.  `--config split1` runs the
-split-history path (one 10k history over all ranks, one all-gather per layer).
+split-history path (one 10k history over all ranks; per layer the partials are read in place from the
+owners' buffers over peer memory, or all-gathered by NCCL with --split-exchange nccl).
 
 The JSON line carries the roofline of the projection AND of the attention kernel
 (per-phase CUDA events recorded by the library on the launching stream, in a
@@ -182,13 +183,26 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def device_align(world):
+    """Aligns the ranks' STREAMS (not only their hosts) right before a timed region: a one-element
+    all-reduce on the current stream completes on every device at about the same time, so host launch
+    skew after the barrier does not enter the device-timed region (it would whenever the ranks' kernels
+    wait for each other, as split-history's do)."""
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.all_reduce(torch.ones(1, device="cuda"))
+
+
 def config_dict(wl, args):
     c = wl.cfg
     L = wl.lengths
     return {"workload": c.name, "requests": int(len(L)), "targets_per_request": int(np.diff(wl.tgt_off)[0]),
             "L_avg": float(L.mean()), "L_max": int(L.max()), "L_infer": c.L_infer, "d": c.d, "h": c.h, "r": c.r,
             "M": c.M, "T": wl.T, "N_t": wl.Nt,
-            "parallelism": (f"split-history over {args.gpus} GPU(s) (NCCL all-gather of partials per layer)"
+            "parallelism": (f"split-history over {args.gpus} GPU(s) ("
+                            + ("partials read in place over peer memory, device-side epoch flags"
+                               if args.split_exchange == "peer" else "NCCL all-gather of partials per layer") + ")"
                             if c.name == "split1" else
                             f"one global request set, LPT-sharded over {args.gpus} GPU(s) (stca_plan_shards), "
                             "no collective on the data path"),
@@ -256,6 +270,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the per-phase profiled pass")
     ap.add_argument("--chunk-keys", type=int, default=0, help="split-K chunk cap in keys (0: library default)")
+    ap.add_argument("--split-exchange", choices=("peer", "nccl"), default="peer",
+                    help="split1 on > 1 GPU: partials read in place over peer memory (stca_split_peer_*, default) "
+                         "or all-gathered by NCCL through the exchange callback")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
@@ -300,7 +317,9 @@ def main():
     model = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, dtype=c.dtype, with_z=c.with_z,
                       device=local, chunk_keys=1280 if split else args.chunk_keys,
                       split_rank=rank if split else 0, split_world=world if split else 1,
-                      exchange=stca.nccl_exchange() if split and world > 1 else None)
+                      exchange=stca.nccl_exchange() if split and world > 1 and args.split_exchange == "nccl" else None)
+    if split and world > 1 and args.split_exchange == "peer":  # partials read in place over NVLink
+        model.split_peer_setup(64 << 20)
     bf16 = c.dtype == "bf16"
     Xh = wl.X_bits.view(np.int16) if bf16 else wl.X
     xth = wl.xt_bits.view(np.int16) if bf16 else wl.xt
@@ -325,6 +344,7 @@ def main():
     with Clocks(local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        device_align(world)
         t_start.record(st)
         for _ in range(K):
             step()
@@ -370,6 +390,7 @@ def main():
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        device_align(world)
         e0.record(st)
         for _ in range(K):  # pipelined serving loop: nothing waits on the host inside it
             model.project_history(Xp, wl.hist_off, stream=st)
@@ -442,6 +463,8 @@ def main():
         if world == 1 and not args.no_oracle:
             line["cpu_baseline"] = oracle_sample(gwl)
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()  # every rank is done with the split-history peer buffers before any handle goes
     model.close()
     if world > 1:
         dist.destroy_process_group()

@@ -49,7 +49,9 @@ typedef enum {
 
 /* Split-history exchange: an all-gather of `bytes` bytes
  * from every rank, called once per layer on `stream` with device pointers.
- * recv holds split_world * bytes bytes, rank-major.  Return 0 on success. */
+ * recv holds split_world * bytes bytes, rank-major.  Return 0 on success.
+ * Optional: handles attached to peer buffers (stca_split_peer_attach) exchange over peer memory
+ * instead and never call it. */
 typedef int (*stca_exchange_fn)(void *ctx, const void *send, void *recv, size_t bytes, void *stream);
 
 /* Device-memory provider for the handle's WORKING buffers (the projected X~ cache, staging, split-K
@@ -73,7 +75,7 @@ typedef struct {
   int32_t split_rank;     /* split-history mode: this rank, 0..split_world-1 */
   int32_t split_world;    /* 1 = off; > 1: every rank gets the SAME full inputs and owns a */
                           /* contiguous block of key chunks of every history */
-  stca_exchange_fn exchange;
+  stca_exchange_fn exchange; /* split-history without peer buffers: the per-layer all-gather */
   void *exchange_ctx;
   stca_alloc_fn dev_alloc; /* NULL: stream-ordered CUDA pool (see stca_alloc_fn) */
   stca_free_fn dev_free;
@@ -348,6 +350,36 @@ typedef struct {
 stca_status stca_encode_history(const stca_embed_tables *tables, int32_t d, int32_t dtype, const int64_t *video_id,
                                 const int64_t *action_id, const int64_t *timestamp, const int64_t *hist_off,
                                 const int64_t *req_time, int64_t B, int64_t T, void *X, void *stream);
+
+/* ---- split-history over peer memory (the LSE merge of P:L289's key chunks over
+ * NVLink / NVSwitch without a collective library) ----
+ * Every rank of a split-history group (split_world = G >= 2) exports ONE exchange buffer of
+ * 4096 + 2 * capacity_bytes bytes (cudaMalloc on the handle's device; capacity rounded up to 4 KB):
+ * 4 KB of epoch flags, then two slots for the per-layer partials (the layer's (O/l, m, l) rows of the
+ * chunks it owns, alternating by layer).  After every rank has exported, each one attaches the G
+ * buffers in rank order (its own at bases[split_rank]; a peer's buffer mapped into this process, e.g.
+ * by stca_ipc_open of the handle the peer exported).  From then on every stca_forward runs, per layer:
+ * attention into this layer's slot -> a one-thread kernel publishes the layer's epoch to every peer
+ * (a system-scope release store into the peer's flag word) and waits until every peer has published it
+ * -> the merge folds each chunk reading it IN PLACE from its owner's slot over NVLink (L2-only loads).  A slot
+ * is rewritten two layers later, which every peer's merge of the layer in between proves safe, so no
+ * second flag exists.  All waits run on the device (one spinning thread per rank; a watchdog traps
+ * after 30 s without a peer, which surfaces as STCA_ERR_CUDA): the host never blocks and the step stays
+ * graph-capturable.
+ * Every rank must issue the same sequence of stca_forward calls; all ranks must stop using the buffers
+ * (e.g. a barrier) before any of them calls stca_destroy.
+ *
+ * stca_split_peer_export: *base_out = the buffer (DEVICE); ipc_handle_out (64 bytes, a
+ *   cudaIpcMemHandle_t) or NULL.  STATE if not in split-history mode or already exported; OOM.
+ * stca_split_peer_attach: bases = G DEVICE pointers valid in this process.  INVALID_ARG if
+ *   bases[split_rank] is not the exported buffer; STATE before export.  A forward whose partials exceed
+ *   capacity_bytes fails with INVALID_ARG before any launch.
+ * stca_ipc_open / stca_ipc_close: map / unmap a peer's exported buffer (cudaIpcOpenMemHandle with lazy
+ *   peer access) on `device`.  STCA_ERR_CUDA on failure. */
+stca_status stca_split_peer_export(stca_handle *h, int64_t capacity_bytes, void **base_out, void *ipc_handle_out);
+stca_status stca_split_peer_attach(stca_handle *h, void *const *bases);
+stca_status stca_ipc_open(const void *ipc_handle, int32_t device, void **ptr_out);
+stca_status stca_ipc_close(void *ptr);
 
 #ifdef __cplusplus
 }

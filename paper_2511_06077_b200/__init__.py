@@ -101,6 +101,7 @@ class STCA:
         """allocator: "torch" (working buffers from PyTorch's caching allocator) or "cuda" (the
         library's stream-ordered CUDA pool)."""
         self.d, self.h, self.r, self.M, self.with_z = d, h, r, M, with_z
+        self._device = device
         self.dtype = dtype
         cfg = _Config()
         cfg.d, cfg.h, cfg.r, cfg.M = d, h, r, M
@@ -147,9 +148,48 @@ class STCA:
 
     # -- lifecycle --
     def close(self):
+        """Destroys the handle.  Split-history over peer memory: every rank must be done with the buffers
+        (a barrier) before any rank closes."""
+        for p in getattr(self, "_ipc", []):
+            lib().stca_ipc_close(ctypes.c_void_p(p))
+        self._ipc = []
         if getattr(self, "_h", None):
             lib().stca_destroy(self._h)
             self._h = None
+
+    # ---- split-history over peer memory (stca_split_peer_*) ----
+    def split_peer_export(self, capacity_bytes: int = 64 << 20):
+        """Allocates this rank's exchange buffer; returns (device address, 64-byte IPC handle)."""
+        base = ctypes.c_void_p()
+        hd = (ctypes.c_uint8 * 64)()
+        self._check(lib().stca_split_peer_export(self._h, int(capacity_bytes), ctypes.byref(base), hd))
+        return int(base.value), bytes(hd)
+
+    def split_peer_attach(self, bases) -> None:
+        """bases: the G ranks' exchange buffers as device addresses valid in this process, rank order."""
+        arr = (ctypes.c_void_p * len(bases))(*[ctypes.c_void_p(int(b)) for b in bases])
+        self._check(lib().stca_split_peer_attach(self._h, arr))
+
+    def split_peer_setup(self, capacity_bytes: int = 64 << 20, group=None) -> None:
+        """One process per GPU (torch.distributed initialised, split_rank == the group rank): export, all-gather
+        the IPC handles (setup only, never on the data path), map the peers' buffers, attach, barrier."""
+        import torch.distributed as dist
+        base, hd = self.split_peer_export(capacity_bytes)
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, hd, group=group)
+        bases, self._ipc = [], []
+        for g, hg in enumerate(handles):
+            if g == rank:
+                bases.append(base)
+                continue
+            ptr = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * 64).from_buffer_copy(hg)
+            self._check(lib().stca_ipc_open(buf, int(self._device), ctypes.byref(ptr)))
+            self._ipc.append(int(ptr.value))
+            bases.append(int(ptr.value))
+        self.split_peer_attach(bases)
+        dist.barrier(group)
 
     def __del__(self):  # pragma: no cover
         try:

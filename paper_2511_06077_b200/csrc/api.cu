@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/stca.h: validation, host planning (exact integer
 // work), device memory ownership and the orchestration of the
 // STCA forward under RLB (§3.1-3.2).  Kernels live in kernels_*.cu / tc_*.cu.
+#include <cuda.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -8,6 +9,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -173,6 +175,14 @@ struct stca_handle {
   // the forward's per-layer U and Y (save_act), the target-side scratch, dX~ of one layer, unrequested gradients
   std::map<std::string, float *> w32;
   bool save_act = false;
+  // split-history over peer memory (stca_split_peer_export / stca_split_peer_attach)
+  void *peer_buf = nullptr;  // this rank's exchange buffer (cudaMalloc): [4 KB: ready[64], device UUID at 1024 | slot 0 | slot 1]
+  int64_t peer_cap = 0;      // bytes per slot
+  bool peer_on = false;
+  void **peer_tab = nullptr;  // device: [slot 0 of rank g][slot 1 of rank g][ready flags of g], G each
+  uint64_t epoch = 0;         // one per layer of every split forward (identical on all ranks)
+  std::vector<uint8_t *> peer_bases;  // host copy of the G buffers' addresses
+  uint8_t peer_uuid[16] = {};         // this device's UUID (also at byte 1024 of the exported buffer)
   DevBuf act, sbwd_scratch, dxt_buf, gsink, dxsink;
   // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
   int cap_layer = 0;
@@ -516,7 +526,7 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
   if (cfg->chunk_keys < 0 || cfg->chunk_keys % 128)
     return bad(fail(h, STCA_ERR_INVALID_ARG, "chunk_keys must be a multiple of 128 (got %d)", cfg->chunk_keys));
   if (cfg->split_world < 0 || cfg->split_world > 64 ||
-      (cfg->split_world > 1 && (cfg->split_rank < 0 || cfg->split_rank >= cfg->split_world || !cfg->exchange)))
+      (cfg->split_world > 1 && (cfg->split_rank < 0 || cfg->split_rank >= cfg->split_world)))
     return bad(fail(h, STCA_ERR_INVALID_ARG, "bad split-history settings (rank %d of %d, exchange %p)",
                     cfg->split_rank, cfg->split_world, (void *)cfg->exchange));
   if (!(cfg->ln_eps > 0.f)) h->cfg.ln_eps = 1e-5f;
@@ -693,6 +703,8 @@ extern "C" void stca_destroy(stca_handle *h) {
   cudaSetDevice(h->cfg.device);
   cudaDeviceSynchronize();
   for (void *p : h->allocs) cudaFree(p);
+  if (h->peer_buf) cudaFree(h->peer_buf);
+  if (h->peer_tab) cudaFree(h->peer_tab);
   int nb = 0;
   DevBuf *const *bufs = all_bufs(h, &nb);
   for (int i = 0; i < nb; ++i) bufs[i]->release();
@@ -1193,6 +1205,37 @@ extern "C" stca_status stca_forward(stca_handle *h, const void *xt, int64_t Nt, 
   return s;
 }
 
+// Split-history epoch exchange as STREAM memory operations (cuStreamWriteValue64 into every peer's flag
+// word -- preceded by a system-wide fence of this stream's earlier writes -- then cuStreamWaitValue64 on
+// this rank's own flag words): the stream front end waits, no SM is held spinning.  False when the driver
+// does not offer them (the caller then launches k_peer_exchange).
+typedef CUresult (*MemOp64Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+static bool peer_exchange_memops(stca_handle *h, uint64_t epoch, cudaStream_t st) {
+  static MemOp64Fn wr = nullptr, wt = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr, *q = nullptr;
+    cudaDriverEntryPointQueryResult r1, r2;
+    if (getenv("STCA_PEER_KERNEL")) return;  // A/B: the one-thread spinning kernel instead
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &r1) == cudaSuccess &&
+        r1 == cudaDriverEntryPointSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue64", &q, cudaEnableDefault, &r2) == cudaSuccess &&
+        r2 == cudaDriverEntryPointSuccess) {
+      wr = (MemOp64Fn)p;
+      wt = (MemOp64Fn)q;
+    }
+  });
+  if (!wr || !wt) return false;
+  const int G = h->cfg.split_world, me = h->cfg.split_rank;
+  for (int g = 0; g < G; ++g)
+    if (g != me && wr((CUstream)st, (CUdeviceptr)(h->peer_bases[g] + 8 * me), epoch, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return false;
+  for (int g = 0; g < G; ++g)
+    if (g != me && wt((CUstream)st, (CUdeviceptr)(h->peer_bases[me] + 8 * g), epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return false;
+  return true;
+}
+
 static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, const int64_t *tgt_off, int64_t B,
                                 float *out_Z, float *out_z, cudaStream_t st) {
   stca_status s = STCA_OK;
@@ -1335,8 +1378,15 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
   stca::MergeItem *d_mitems = reinterpret_cast<stca::MergeItem *>(h->plan.as<uint8_t>() + mi_at);
   int32_t *d_ctal = reinterpret_cast<int32_t *>(h->plan.as<uint8_t>() + ctal_at);
   const size_t part_bytes = (size_t)part_rows * stca::part_row_bytes(d, es);
-  if (part_rows) CU(h->part.ensure(part_bytes, st));
-  if (G > 1 && part_rows) CU(h->partg.ensure(part_bytes * G, st));
+  const bool peer = G > 1 && h->peer_on;
+  if (G > 1 && !peer && !h->cfg.exchange)
+    return fail(h, STCA_ERR_INVALID_ARG, "split-history needs an exchange callback or attached peer buffers");
+  if (peer && (int64_t)part_bytes > h->peer_cap)
+    return fail(h, STCA_ERR_INVALID_ARG, "the partials (%zu bytes) exceed the peer buffer slot (%lld bytes)", part_bytes,
+                (long long)h->peer_cap);
+  if (part_rows && !peer) CU(h->part.ensure(part_bytes, st));
+  if (G > 1 && part_rows && !peer) CU(h->partg.ensure(part_bytes * G, st));
+  const uint64_t *const flags_ready = peer ? (const uint64_t *)h->peer_buf : nullptr;
 
   // target side: at d = 128 every layer boundary is ONE fused kernel (tc_chain.cu: o(i) -> Z, ocat;
   // c = [..] W_C; q = SwiGLUFFN(c); U = q W_QK), otherwise separate tcgen05 GEMMs / CUDA-core kernels
@@ -1382,31 +1432,48 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       if (s != STCA_OK) return s;
     }
     // a4: ragged single-query attention per request, reordered form Eq.(13)
+    float *part_i = h->part.as<float>();
+    uint64_t epoch = 0;
+    if (peer) {  // this layer's slot of the exchange buffer (the peers read it two layers ago: see below)
+      epoch = ++h->epoch;
+      part_i = (float *)((uint8_t *)h->peer_buf + 4096 + (size_t)(epoch & 1) * h->peer_cap);
+    }
     cudaEvent_t pa = prof_begin(h, st);
     for (int rep = 0; rep < h->reps_attn; ++rep) {  // idempotent (STCA_PROF_TWICE_ATTENTION)
     if (tc_attn) {
       if (nit_nar > 0)
         CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, d_items + nit_reg,
                                      d_ctal + nar_at, d_ctal + nar_at + n_ctas_nar + 1,
-                                     n_ctas_nar, h->Y.p, h->part.as<float>(), st));
+                                     n_ctas_nar, h->Y.p, part_i, st));
       if (nit_reg > 0)
         CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, d_items, d_ctal,
-                            d_ctal + n_ctas + 1, n_ctas, d, h->Y.p, h->part.as<float>(), st));
+                            d_ctal + n_ctas + 1, n_ctas, d, h->Y.p, part_i, st));
     } else if (tc_wide) {
 #ifdef STCA_PAIR_ATTN
       CU(stca::tc_attention_pair(h->U.p, NQ, Xt, h->T2, d_items, nit, d, h->Y.p,
-                                 h->part.as<float>(), st));
+                                 part_i, st));
 #else
       CU(stca::tc_attention_wide(h->U.p, NQ, Xt, h->T2, d_items, nit, d, h->Y.p,
-                                 h->part.as<float>(), st));
+                                 part_i, st));
 #endif
     } else {
-      CU(stca::cc_attention(h->bf16, h->U.p, Xt, d_items, nit, d, h->Y.p, h->part.as<float>(), st));
+      CU(stca::cc_attention(h->bf16, h->U.p, Xt, d_items, nit, d, h->Y.p, part_i, st));
     }
     }
     prof_end(h, STCA_PH_ATTENTION, pa, st);
-    const float *merged_from = h->part.as<float>();
-    if (G > 1 && part_rows) {  // split-history exchange: all-gather every rank's partials (one step per layer)
+    const float *merged_from = part_i;
+    // split-history over peer memory: one 1-thread kernel publishes this layer's epoch and waits for every
+    // peer's, then the merge reads each chunk in place.  Slot reuse needs no second flag: this rank overwrites slot (e & 1)
+    // in layer e + 2 only after its merge of e + 1 saw every peer's epoch e + 1, which a peer publishes
+    // only after its own merge of e (the one reading this slot) has completed (stream order + PDL waits).
+    stca::PeerMerge pmg{};
+    if (peer) {
+      pmg.slots = (const uint8_t *const *)(h->peer_tab + (epoch & 1) * G);
+      pmg.ready_remote = (uint64_t *const *)(h->peer_tab + 2 * G);
+      pmg.ready_local = flags_ready;
+      pmg.me = grank;
+      pmg.epoch = epoch;
+    } else if (G > 1 && part_rows) {  // split-history exchange: all-gather every rank's partials (one step per layer)
       if (h->cfg.exchange(h->cfg.exchange_ctx, h->part.p, h->partg.p, part_bytes, (void *)st) != 0)
         return fail(h, STCA_ERR_COMM, "split-history exchange failed at layer %d", i);
       merged_from = h->partg.as<float>();
@@ -1418,8 +1485,11 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       CU(cudaMemcpyAsync(h->act.as<uint8_t>() + (size_t)2 * (i - 1) * NQ * d * es, h->U.p, (size_t)NQ * d * es,
                          cudaMemcpyDeviceToDevice, st));
     pa = prof_begin(h, st);
-    CU(stca::merge_partials(h->bf16, d_mitems, (int64_t)mi.size(), max_rows, max_chunks, merged_from, d,
-                            G, (int64_t)part_bytes, h->Y.p, st));
+    if (peer) {  // publish this layer's epoch to every peer, then wait (in the stream) for every peer's
+      if (!peer_exchange_memops(h, epoch, st)) CU(stca::peer_exchange(pmg, G, st));
+    }
+    CU(stca::merge_partials(h->bf16, d_mitems, (int64_t)mi.size(), max_rows, max_chunks, merged_from,
+                            peer ? &pmg : nullptr, d, G, (int64_t)part_bytes, h->Y.p, st));
     if (!mi.empty()) prof_end(h, STCA_PH_MERGE, pa, st);
     else if (pa) h->prof_pool.push_back(pa);
     if (h->cap_layer == i) {
@@ -1798,5 +1868,87 @@ extern "C" stca_status stca_backward(stca_handle *h, const void *xt, int64_t Nt,
   a.ctx = &c;
   a.scratch = h->sbwd_scratch.p;
   CU(stca::stack_bwd(&h->blas, a, st));
+  return STCA_OK;
+}
+
+// ===========================================================================
+// split-history over peer memory (NVLink / NVSwitch): one exchange buffer per rank, read in place by
+// every peer's merge kernel; epoch flags instead of a collective
+// ===========================================================================
+extern "C" stca_status stca_split_peer_export(stca_handle *h, int64_t capacity_bytes, void **base_out,
+                                              void *ipc_handle_out) {
+  if (!h || !base_out || capacity_bytes <= 0) return STCA_ERR_INVALID_ARG;
+  if (h->cfg.split_world < 2) return fail(h, STCA_ERR_STATE, "peer buffers need split-history mode (split_world >= 2)");
+  if (h->peer_buf) return fail(h, STCA_ERR_STATE, "the peer buffer was already exported");
+  CU(cudaSetDevice(h->cfg.device));
+  const int64_t cap = (capacity_bytes + 4095) / 4096 * 4096;
+  void *p = nullptr;
+  if (cudaMalloc(&p, (size_t)(4096 + 2 * cap)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, STCA_ERR_OOM, "peer buffer of %lld bytes", (long long)(4096 + 2 * cap));
+  }
+  h->peer_buf = p;
+  h->peer_cap = cap;
+  CU(cudaMemset(p, 0, 4096));  // epoch flags start at 0 (synchronous: before any peer can see the buffer)
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, h->cfg.device));
+  memcpy(h->peer_uuid, &prop.uuid, 16);
+  CU(cudaMemcpy((uint8_t *)p + 1024, h->peer_uuid, 16, cudaMemcpyHostToDevice));  // read by the peers' attach
+  if (ipc_handle_out) CU(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)ipc_handle_out, p));
+  *base_out = p;
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_split_peer_attach(stca_handle *h, void *const *bases) {
+  if (!h || !bases) return STCA_ERR_INVALID_ARG;
+  const int G = h->cfg.split_world, me = h->cfg.split_rank;
+  if (!h->peer_buf) return fail(h, STCA_ERR_STATE, "stca_split_peer_attach before stca_split_peer_export");
+  if (bases[me] != h->peer_buf) return fail(h, STCA_ERR_INVALID_ARG, "bases[%d] is not this rank's exported buffer", me);
+  std::vector<void *> tab((size_t)3 * G);
+  for (int g = 0; g < G; ++g) {
+    if (!bases[g]) return fail(h, STCA_ERR_INVALID_ARG, "bases[%d] is NULL", g);
+    if (g != me) {  // the exporter wrote its device's UUID at byte 1024 of its buffer
+      uint8_t uu[16];
+      if (cudaMemcpy(uu, (const uint8_t *)bases[g] + 1024, 16, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, STCA_ERR_INVALID_ARG, "bases[%d] is not readable from this process", g);
+      }
+      if (memcmp(uu, h->peer_uuid, 16) == 0)
+        return fail(h, STCA_ERR_UNSUPPORTED,
+                    "peer exchange needs one rank per device (rank %d is on this rank's device): ranks sharing a "
+                    "device wait for each other inside their streams and can serialise on its work queues", g);
+    }
+    uint8_t *b = (uint8_t *)bases[g];
+    tab[g] = b + 4096;
+    tab[G + g] = b + 4096 + h->peer_cap;
+    tab[2 * G + g] = b;  // ready flags of rank g
+  }
+  CU(cudaSetDevice(h->cfg.device));
+  if (!h->peer_tab) CU(cudaMalloc((void **)&h->peer_tab, tab.size() * sizeof(void *)));
+  CU(cudaMemcpy(h->peer_tab, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice));
+  h->peer_bases.assign((uint8_t *const *)bases, (uint8_t *const *)bases + G);
+  h->peer_on = true;
+  h->epoch = 0;
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_ipc_open(const void *ipc_handle, int32_t device, void **ptr_out) {
+  if (!ipc_handle || !ptr_out) return STCA_ERR_INVALID_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return STCA_ERR_CUDA;
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, ipc_handle, sizeof hd);
+  if (cudaIpcOpenMemHandle(ptr_out, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return STCA_ERR_CUDA;
+  }
+  return STCA_OK;
+}
+
+extern "C" stca_status stca_ipc_close(void *ptr) {
+  if (!ptr) return STCA_ERR_INVALID_ARG;
+  if (cudaIpcCloseMemHandle(ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return STCA_ERR_CUDA;
+  }
   return STCA_OK;
 }

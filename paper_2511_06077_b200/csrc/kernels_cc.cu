@@ -2,6 +2,9 @@
 // utility kernels shared by both paths.  SURVEY §2.2 K-G; Eq.(1)-(9).
 #include <math.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "launch.h"
 
 namespace stca {
@@ -265,46 +268,84 @@ cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const Attn
 // its owner rank floor(c G / C); with G = 1 this is the intra-GPU split-K merge.
 // grid: (items, row blocks of 8 rows), warp per row.
 // --------------------------------------------------------------------------
-template <typename S>
-__device__ __forceinline__ float4 load4(const uint8_t *p);
-template <>
-__device__ __forceinline__ float4 load4<float>(const uint8_t *p) {
-  return __ldg(reinterpret_cast<const float4 *>(p));
-}
-template <>
-__device__ __forceinline__ float4 load4<bf16>(const uint8_t *p) {
-  const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
-  return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u), __uint_as_float(v.y << 16),
-                     __uint_as_float(v.y & 0xffff0000u));
+// PEER: the bytes live in another GPU's memory (written there by its own kernels), read through NVLink
+// with L2-only loads (ld.global.cg) -- the SM's L1 is not coherent with a peer's writes, and a slot is
+// reused every second layer
+template <typename S, bool PEER>
+__device__ __forceinline__ float4 load4(const uint8_t *p) {
+  if constexpr (sizeof(S) == 4) {
+    return PEER ? __ldcg(reinterpret_cast<const float4 *>(p)) : __ldg(reinterpret_cast<const float4 *>(p));
+  } else {
+    const uint2 v = PEER ? __ldcg(reinterpret_cast<const uint2 *>(p)) : __ldg(reinterpret_cast<const uint2 *>(p));
+    return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u), __uint_as_float(v.y << 16),
+                       __uint_as_float(v.y & 0xffff0000u));
+  }
 }
 
-template <typename S, int MAXC, int RPW>
+// split-history over peer memory: epoch flags between the ranks' kernels (no host, no collective
+// library).  Rank g's flag words live in its own exchange buffer: ready[src] = the last epoch (layer
+// of a forward) whose partials rank src has published.  A signal is one system-scope release store per
+// peer after a system-scope fence; a wait spins on the rank's OWN memory with acquire loads.  A watchdog
+// traps after 30 s without the peer (a peer that never arrives must not hang the GPU).
+__device__ __forceinline__ void peer_signal_all(uint64_t *const *remote, int G, int me, uint64_t epoch) {
+  __threadfence_system();
+  for (int g = 0; g < G; ++g)
+    if (g != me) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote[g] + me), "l"(epoch) : "memory");
+}
+
+__device__ __forceinline__ void peer_wait_all(const uint64_t *flags, int G, int me, uint64_t target) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int g = 0; g < G; ++g) {
+    if (g == me) continue;
+    for (;;) {
+      uint64_t v, t;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + g) : "memory");
+      if ((int64_t)v >= (int64_t)target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 30000000000ull) {  // 30 s without the peer: fail loudly instead of hanging
+        printf("stca peer wait: rank %d epoch %llu: rank %d is at %llu\n", me, (unsigned long long)target, g,
+               (unsigned long long)v);
+        __trap();
+      }
+      __nanosleep(32);
+    }
+  }
+}
+
+template <typename S, int MAXC, int RPW, bool PEER>
 __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ items, const uint8_t *__restrict__ part,
-                                                int d, int G, int64_t rank_stride, S *__restrict__ Y) {
+                                                const PeerMerge pm_, int d, int G, int64_t rank_stride,
+                                                S *__restrict__ Y) {
   // MAXC: chunks per request handled in registers (C <= MAXC); RPW: rows per warp, all of their
   // loads issued before any use (the merge is latency-bound: more bytes in flight per thread)
   pdl_wait();  // the attention's partials are complete and visible
   pdl_trigger();
+  const uint8_t *const *peer = pm_.slots;  // PEER: k_peer_exchange (the previous kernel) saw every peer's epoch
   const MergeItem it = items[blockIdx.x];
   const int lane = threadIdx.x % 32;
   const int qw = (blockIdx.y * 8 + threadIdx.x / 32) * RPW;  // this warp's first row
   if (qw >= it.rows) return;
   const int64_t rb = part_row_bytes(d, sizeof(S));
   const int64_t stride = (int64_t)it.rows * rb;
-  int64_t off[MAXC];  // chunk c's partial lives in rank floor(c G / C)'s buffer
+  const uint8_t *cb[MAXC];  // chunk c's partial lives in rank floor(c G / C)'s buffer (PEER: its own memory)
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) off[c] = c < it.nchunks ? (int64_t)((c * G) / it.nchunks) * rank_stride + c * stride : 0;
+  for (int c = 0; c < MAXC; ++c) {
+    const int src = c < it.nchunks ? (c * G) / it.nchunks : 0;
+    cb[c] = (PEER ? peer[src] : part + (int64_t)src * rank_stride) + (c < it.nchunks ? c * stride : 0);
+  }
   const int e0 = lane * 4;
   float2 ml[RPW][MAXC];  // (m, l) of every row and chunk
   float4 a0[RPW][MAXC];  // and the first 128 output columns
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
-    const uint8_t *p0 = part + (it.part_row + qw + r) * rb;
+    const int64_t r0 = (it.part_row + qw + r) * rb;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (qw + r < it.rows && c < it.nchunks) {
-        ml[r][c] = __ldg(reinterpret_cast<const float2 *>(p0 + off[c] + d * sizeof(S)));
-        if (e0 < d) a0[r][c] = load4<S>(p0 + off[c] + e0 * sizeof(S));
+        const float2 *pm = reinterpret_cast<const float2 *>(cb[c] + r0 + d * sizeof(S));
+        ml[r][c] = PEER ? __ldcg(pm) : __ldg(pm);
+        if (e0 < d) a0[r][c] = load4<S, PEER>(cb[c] + r0 + e0 * sizeof(S));
       }
     }
   }
@@ -312,7 +353,7 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
   for (int r = 0; r < RPW; ++r) {
     const int q = qw + r;
     if (q >= it.rows) break;
-    const uint8_t *p0 = part + (it.part_row + q) * rb;
+    const int64_t r0 = (it.part_row + q) * rb;
     float mu = -INFINITY;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c)
@@ -332,7 +373,7 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         if (c < it.nchunks) {
-          const float4 a = e == e0 ? a0[r][c] : load4<S>(p0 + off[c] + e * sizeof(S));
+          const float4 a = e == e0 ? a0[r][c] : load4<S, PEER>(cb[c] + r0 + e * sizeof(S));
           acc.x += w[c] * a.x;
           acc.y += w[c] * a.y;
           acc.z += w[c] * a.z;
@@ -353,15 +394,20 @@ __global__ void __launch_bounds__(256) k_merge(const MergeItem *__restrict__ ite
 }
 
 cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, int max_chunks,
-                           const float *part, int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st) {
+                           const float *part, const PeerMerge *peer, int d, int G, int64_t rank_stride_bytes, void *Y,
+                           cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   const uint8_t *p = (const uint8_t *)part;
+  const PeerMerge pm = peer ? *peer : PeerMerge{};
   note_launch();
-#define STCA_MERGE(S, MC, RPW)                                                                                    \
-  do {                                                                                                           \
-    cudaError_t e = launch_pdl(k_merge<S, MC, RPW>, dim3((unsigned)n_items, (unsigned)((max_rows + 8 * RPW - 1) / (8 * RPW))), \
-                               dim3(256), 0, st, items, p, d, G, rank_stride_bytes, (S *)Y);                       \
-    if (e != cudaSuccess) return e;                                                                              \
+#define STCA_MERGE(S, MC, RPW)                                                                                      \
+  do {                                                                                                             \
+    const dim3 grid((unsigned)n_items, (unsigned)((max_rows + 8 * RPW - 1) / (8 * RPW)));                          \
+    cudaError_t e = peer ? launch_pdl(k_merge<S, MC, RPW, true>, grid, dim3(256), 0, st, items, p, pm, d, G,        \
+                                      rank_stride_bytes, (S *)Y)                                                   \
+                         : launch_pdl(k_merge<S, MC, RPW, false>, grid, dim3(256), 0, st, items, p, pm, d, G,       \
+                                      rank_stride_bytes, (S *)Y);                                                  \
+    if (e != cudaSuccess) return e;                                                                                \
   } while (0)
   if (max_chunks <= 2) {  // the common case (a 10k history at the default cap): 4 rows per warp
     if (is_bf16) STCA_MERGE(bf16, 2, 4);
@@ -371,6 +417,24 @@ cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items
     else STCA_MERGE(float, 8, 1);
   }
 #undef STCA_MERGE
+  return cudaGetLastError();
+}
+
+// Fallback of the stream memory operations (api.cu peer_exchange_memops, STCA_PEER_KERNEL=1): publish
+// this rank's epoch (its partials are complete: the attention kernel before it in the stream), then wait
+// until every peer has published it; one thread of one CTA spins.
+__global__ void k_peer_exchange(uint64_t *const *__restrict__ remote, const uint64_t *__restrict__ local, int G, int me,
+                                uint64_t epoch) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    peer_signal_all(remote, G, me, epoch);
+    peer_wait_all(local, G, me, epoch);
+  }
+}
+
+cudaError_t peer_exchange(const PeerMerge &pm, int G, cudaStream_t st) {
+  note_launch();
+  k_peer_exchange<<<1, 32, 0, st>>>(pm.ready_remote, pm.ready_local, G, pm.me, pm.epoch);
   return cudaGetLastError();
 }
 

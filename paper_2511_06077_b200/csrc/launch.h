@@ -56,9 +56,20 @@ cudaError_t cc_layernorm(bool is_bf16, const float *in, int64_t ldi, const float
 // online-softmax sweep over items (qtile <= 16 rows per item)
 cudaError_t cc_attention(bool is_bf16, const void *U, const void *Xt, const AttnItem *items, int64_t n_items, int d,
                          void *Y, float *part, cudaStream_t st);
+// split-history over peer memory: peer_exchange publishes this rank's epoch and waits for every peer's
+// (one spinning thread), then the merge reads chunk c from its owner's slot in place (kernels_cc.cu)
+struct PeerMerge {
+  const uint8_t *const *slots;   // device table: G ranks' partial slots of this epoch
+  uint64_t *const *ready_remote; // device table: G ranks' ready-flag arrays
+  const uint64_t *ready_local;   // this rank's ready flags (written by the peers)
+  int me;
+  uint64_t epoch;
+};
+// peer: NULL (part holds G rank-major copies when G > 1), or the peer-memory exchange of this layer
 cudaError_t merge_partials(bool is_bf16, const MergeItem *items, int64_t n_items, int max_rows, int max_chunks,
-                           const float *part,
-                           int d, int G, int64_t rank_stride_bytes, void *Y, cudaStream_t st);
+                           const float *part, const PeerMerge *peer, int d, int G, int64_t rank_stride_bytes,
+                           void *Y, cudaStream_t st);
+cudaError_t peer_exchange(const PeerMerge &pm, int G, cudaStream_t st);
 
 // ---- history-path backward (hist_bwd.cu; NEXT-1 partial) ----
 size_t hist_bwd_scratch_bytes(int d, int rd, int64_t R);

@@ -68,6 +68,33 @@ def test_split_history_threads_bit_exact(G, m):
     assert rowrel(Z1, Zr).max() <= 2e-2 and rowrel(z1, zr).max() <= 2e-2
 
 
+def test_split_peer_errors():
+    import paper_2511_06077_b200 as stca
+    wl = split_workload(8)
+    m1 = _model(wl)
+    with pytest.raises(stca.StcaError):  # not in split-history mode
+        m1.split_peer_export(1 << 20)
+    a, b = _model(wl, split_rank=0, split_world=2), _model(wl, split_rank=1, split_world=2)
+    with pytest.raises(stca.StcaError):  # attach before export
+        a.split_peer_attach([0, 0])
+    ba, bb = a.split_peer_export(4096)[0], b.split_peer_export(4096)[0]
+    with pytest.raises(stca.StcaError):  # own buffer not at bases[rank]
+        a.split_peer_attach([bb, ba])
+    with pytest.raises(stca.StcaError):  # both ranks on one device: refused (they would wait inside one GPU)
+        a.split_peer_attach([ba, bb])
+
+
+@pytest.mark.skipif("not __import__('torch').cuda.is_available() or __import__('torch').cuda.device_count() < 2")
+def test_split_history_peer_two_gpus():
+    """Peer memory across processes (CUDA IPC handles exchanged once at setup, NVLink reads), 2 GPUs."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(root, "tools", "split_nccl.py"),
+                        "--peer"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "split_nccl ok" in r.stdout
+
+
 @pytest.mark.skipif("not __import__('torch').cuda.is_available() or __import__('torch').cuda.device_count() < 2")
 def test_split_history_nccl_two_gpus():
     """The same over NCCL on 2 GPUs (torchrun, one process per GPU)."""

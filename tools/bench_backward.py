@@ -85,6 +85,37 @@ def main():
         hist = {"kernel": "history-path backward (stca_history_backward, one layer; cuBLAS GEMMs + kernels)",
                 "ms_per_call": hms, "achieved_TFLOPs": hfl / (hms * 1e-3) / 1e12,
                 "frac_of_bf16_peak": hfl / (hms * 1e-3) / 1e12 / pk["bf16_tflops"], "algorithmic_flops": hfl}
+    # the whole-stack backward (stca_backward: forward with saved U / Y + every layer's backward), one call
+    full = None
+    if Xk is not None and int(Xk.shape[0]) == T2:
+        dZ = torch.randn(wl.Nt, c.M, c.d, device="cuda")
+        dz = torch.randn(wl.Nt, c.d, device="cuda")
+        grads = {n: torch.empty(tuple(sh), device="cuda") for n, sh in m._shapes.items()}
+        dXs = torch.empty(T2, c.d, device="cuda")
+        dxts = torch.empty(wl.Nt, c.d, device="cuda")
+        Zs = torch.empty(wl.Nt, c.M, c.d, device="cuda")
+        for _ in range(2):
+            m.backward(xt, wl.tgt_off, Xk, dZ, dz, grads=grads, dX=dXs, dxt=dxts, out_Z=Zs, stream=st)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(st)
+        for _ in range(3):
+            m.backward(xt, wl.tgt_off, Xk, dZ, dz, grads=grads, dX=dXs, dxt=dxts, out_Z=Zs, stream=st)
+        f1.record(st)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / 3
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(st)
+        for _ in range(3):
+            m.project_history(X, wl.hist_off, stream=st)
+        p1.record(st)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / 3
+        full = {"call": "stca_backward (forward keeping U / Y, then the backward of all layers: target side, "
+                        "attention, history path; every weight role, dX, dx_t)",
+                "ms_per_call": fms, "project_ms": pms,
+                "train_step_ms": pms + fms, "train_targets_per_s": wl.Nt / ((pms + fms) * 1e-3),
+                "timing": "CUDA events on the launching stream, 3 calls after 2 warm-up calls"}
     print(json.dumps({"kernel": "attention backward (stca_attention_backward, one layer)", "config": a.config,
                       "ms_per_launch": ms, "targets_per_s": wl.Nt / (ms * 1e-3),
                       "roofline": {"bound": bound, "achieved": ach, "peak": peak,
@@ -92,7 +123,7 @@ def main():
                                    "algorithmic_flops": flops, "algorithmic_bytes": byts,
                                    "note": "the kernel reads X~ twice (pass 1: softmax statistics; pass 2: "
                                            "gradients): algorithmic bytes count it once"},
-                      "T": T2, "N_t": wl.Nt, "history_backward": hist}), flush=True)
+                      "T": T2, "N_t": wl.Nt, "history_backward": hist, "stack_backward": full}), flush=True)
     m.close()
 
 

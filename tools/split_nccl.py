@@ -1,6 +1,7 @@
-"""Split-history over NCCL (run with torchrun, one rank per GPU): every rank gets the same
-inputs, owns a block of each history's key chunks, and the per-layer partials are all-gathered
-through torch.distributed; rank 0 checks bit-exactness against its own unsplit run."""
+"""Split-history across processes (run with torchrun, one rank per GPU): every rank gets the same
+inputs, owns a block of each history's key chunks; the per-layer partials are all-gathered through
+torch.distributed (default) or, with --peer, read in place over peer memory (stca_split_peer_*, CUDA IPC
+handles exchanged once); rank 0 checks bit-exactness against its own unsplit run."""
 import os
 import sys
 
@@ -33,15 +34,32 @@ def main():
         torch.cuda.synchronize()
         return Z, z
 
+    peer = "--peer" in sys.argv
     ms = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, chunk_keys=1280, device=local,
-                   split_rank=rank, split_world=world, exchange=stca.nccl_exchange())
+                   split_rank=rank, split_world=world, exchange=None if peer else stca.nccl_exchange())
+    if peer:  # exchange over peer memory: IPC handles once, then device-side epoch flags only
+        small = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, chunk_keys=1280, device=local,
+                          split_rank=rank, split_world=world)
+        small.split_peer_setup(4096)  # a slot too small for this workload's partials: refused before any launch
+        try:
+            run(small)
+            raise SystemExit("split_nccl: an over-capacity peer forward was not refused")
+        except stca.StcaError:
+            pass
+        dist.barrier()
+        small.close()
+        ms.split_peer_setup(8 << 20)
     Zs, zs = run(ms)
+    Zs2, zs2 = run(ms)  # second forward: the other slot, and the reuse wait
+    same2 = torch.equal(Zs, Zs2) and torch.equal(zs, zs2)
     m1 = stca.STCA(W, d=c.d, h=c.h, r=c.r, M=c.M, L_infer=c.L_infer, chunk_keys=1280, device=local)
     Z1, z1 = run(m1)
-    ok = torch.tensor([int(torch.equal(Zs, Z1) and torch.equal(zs, z1))], device="cuda")
+    ok = torch.tensor([int(torch.equal(Zs, Z1) and torch.equal(zs, z1) and same2)], device="cuda")
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if rank == 0:
         print("split_nccl ok" if int(ok) == 1 else "split_nccl MISMATCH", flush=True)
+    dist.barrier()  # every rank is done with the peer buffers before any handle is destroyed
+    ms.close()
     dist.destroy_process_group()
     sys.exit(0 if int(ok) == 1 else 1)
 
