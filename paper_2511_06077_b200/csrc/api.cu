@@ -130,7 +130,7 @@ struct ProfRegion {
 struct LayerW {
   void *W1h = nullptr, *Woh = nullptr;  // history FFN: [d x 2rd] interleaved (u_j, v_j), [rd x d]
   float *gh = nullptr, *bh = nullptr;
-  void *Wu = nullptr, *Wv = nullptr;    // history FFN Wu, Wv [d x rd] row-major (the backward's GEMMs)
+  void *W1cat = nullptr;                // history FFN [Wu | Wv] [d x 2rd] row-major (the backward's GEMMs)
   void *W1q = nullptr, *Woq = nullptr;  // query FFN
   float *gq = nullptr, *bq = nullptr;   // layer 1 only
   void *WQK = nullptr;                  // [d x h d], scaled by log2(e)/sqrt(d_h)
@@ -606,8 +606,16 @@ extern "C" stca_status stca_create(const stca_config *cfg, const stca_tensor *w,
     LayerW &Ly = h->L[i - 1];
     std::string p = "L" + std::to_string(i) + ".";
     if (!ffn(p + "hist", &Ly.W1h, &Ly.Woh, &Ly.tc)) return bad(fail(h, STCA_ERR_OOM, "upload failed (%s)", p.c_str()));
-    if (!(Ly.Wu = upload(h, W(p + "hist.Wu"), (size_t)d * rd)) || !(Ly.Wv = upload(h, W(p + "hist.Wv"), (size_t)d * rd)))
-      return bad(fail(h, STCA_ERR_OOM, "upload failed (%shist.Wu/Wv)", p.c_str()));
+    {  // [Wu | Wv] column blocks, bf16 [d x 2rd]: the history backward's recompute and dX GEMMs
+      const float *u = W(p + "hist.Wu"), *v = W(p + "hist.Wv");
+      std::vector<float> cat((size_t)d * 2 * rd);
+      for (int e = 0; e < d; ++e) {
+        memcpy(&cat[(size_t)e * 2 * rd], u + (size_t)e * rd, sizeof(float) * rd);
+        memcpy(&cat[(size_t)e * 2 * rd + rd], v + (size_t)e * rd, sizeof(float) * rd);
+      }
+      if (!(Ly.W1cat = upload(h, cat.data(), cat.size())))
+        return bad(fail(h, STCA_ERR_OOM, "upload failed (%shist.Wu/Wv)", p.c_str()));
+    }
     if (W(p + "qry.Wu") == W(p + "hist.Wu") && W(p + "qry.Wv") == W(p + "hist.Wv") && W(p + "qry.Wo") == W(p + "hist.Wo")) {
       Ly.W1q = Ly.W1h;
       Ly.Woq = Ly.Woh;
@@ -1672,7 +1680,7 @@ extern "C" stca_status stca_history_backward(stca_handle *h, int32_t layer, cons
   const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
   CU(h->bwd_scratch.ensure(stca::hist_bwd_scratch_bytes(d, rd, R), st));
   LayerW &Ly = h->L[layer - 1];
-  CU(stca::hist_bwd(&h->blas, (const bf16 *)X, rows, d, rd, (const bf16 *)Ly.Wu, (const bf16 *)Ly.Wv,
+  CU(stca::hist_bwd(&h->blas, (const bf16 *)X, rows, d, rd, (const bf16 *)Ly.W1cat,
                     (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, dX, dWu, dWv, dWo, dgamma, dbeta,
                     h->bwd_scratch.p, R, st));
   return STCA_OK;
@@ -1707,7 +1715,7 @@ static cudaError_t bwd_attn_hist(void *ctx, int layer, const float *dY, float *d
     return e;
   const int64_t R = std::min<int64_t>(std::max<int64_t>(c.rows, 1), 1 << 16);
   LayerW &Ly = h->L[L];
-  return stca::hist_bwd(&h->blas, (const bf16 *)c.X, c.rows, d, rd, (const bf16 *)Ly.Wu, (const bf16 *)Ly.Wv,
+  return stca::hist_bwd(&h->blas, (const bf16 *)c.X, c.rows, d, rd, (const bf16 *)Ly.W1cat,
                         (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, c.dX, c.gWu[L], c.gWv[L], c.gWo[L], c.gg[L],
                         c.gb[L], h->bwd_scratch.p, R, c.st);
 }

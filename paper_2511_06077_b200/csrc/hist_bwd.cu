@@ -8,7 +8,9 @@
 //   k_ln_bwd       per row: mu, s from y; x^ = (y - mu) / s; dx^ = dX~ * gamma;
 //                  dy = (dx^ - mean(dx^) - x^ mean(dx^ x^)) / s -> bf16; dgamma += dX~ x^, dbeta += dX~
 //   k_swiglu_bwd   da = dH silu(g), dg = dH a sig(g) (1 + g (1 - sig(g))) -> bf16
-// Rows are processed in blocks of 2^16 (working set ~0.7 GB at d = 128, r = 4).  Every history row
+// The intermediates are bf16 (a and g come out of ONE GEMM with [Wu | Wv], rounded like the forward's
+// operands), y stays fp32 for the LayerNorm statistics.  Rows are processed in blocks of 2^16 (working
+// set ~0.5 GB at d = 128, r = 4).  Every history row
 // appears once per request however many targets share it, so the gradients are aggregated at the
 // request level by construction.
 #include <cublas_v2.h>
@@ -22,91 +24,142 @@ namespace stca {
 
 namespace {
 
-__global__ void k_swiglu_fwd(const float *__restrict__ a, const float *__restrict__ g, bf16 *__restrict__ h, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gv = g[i];
-    h[i] = __float2bfloat16_rn(a[i] * (gv / (1.f + __expf(-gv))));
+__device__ __forceinline__ float silu_(float g) { return g / (1.f + __expf(-g)); }
+
+// ag = [a | g] bf16 [n x 2rd] (a = X Wu, g = X Wv from one GEMM) -> h = a silu(g) bf16 [n x rd];
+// 8 bf16 (16 bytes) per thread and access, rd % 8 == 0
+__global__ void __launch_bounds__(256) k_swiglu_fwd(const bf16 *__restrict__ ag, bf16 *__restrict__ h, int rd, int64_t n) {
+  const int per_row = rd / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per_row; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per_row;
+    const int j = (int)(i - r * per_row);
+    const uint4 av = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + 8 * j);
+    const uint4 gv = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + rd + 8 * j);
+    const __nv_bfloat162 *a2 = reinterpret_cast<const __nv_bfloat162 *>(&av), *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv);
+    uint4 out;
+    __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(&out);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(a2[k]), g = __bfloat1622float2(g2[k]);
+      o2[k] = __floats2bfloat162_rn(a.x * silu_(g.x), a.y * silu_(g.y));
+    }
+    *reinterpret_cast<uint4 *>(h + r * rd + 8 * j) = out;
   }
 }
 
-__global__ void k_swiglu_bwd(const float *__restrict__ a, const float *__restrict__ g, const float *__restrict__ dh,
-                             bf16 *__restrict__ da, bf16 *__restrict__ dg, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gv = g[i], sg = 1.f / (1.f + __expf(-gv)), d = dh[i];
-    da[i] = __float2bfloat16_rn(d * gv * sg);
-    dg[i] = __float2bfloat16_rn(d * a[i] * sg * (1.f + gv * (1.f - sg)));
+// dag = [da | dg] bf16 [n x 2rd]: da = dH silu(g), dg = dH a sig(g) (1 + g (1 - sig(g)))
+__global__ void __launch_bounds__(256) k_swiglu_bwd(const bf16 *__restrict__ ag, const bf16 *__restrict__ dh,
+                                                    bf16 *__restrict__ dag, int rd, int64_t n) {
+  const int per_row = rd / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per_row; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per_row;
+    const int j = (int)(i - r * per_row);
+    const uint4 av = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + 8 * j);
+    const uint4 gv = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + rd + 8 * j);
+    const uint4 dv = *reinterpret_cast<const uint4 *>(dh + r * rd + 8 * j);
+    const __nv_bfloat162 *a2 = reinterpret_cast<const __nv_bfloat162 *>(&av), *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv),
+                         *d2 = reinterpret_cast<const __nv_bfloat162 *>(&dv);
+    uint4 oa, og;
+    __nv_bfloat162 *oa2 = reinterpret_cast<__nv_bfloat162 *>(&oa), *og2 = reinterpret_cast<__nv_bfloat162 *>(&og);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(a2[k]), g = __bfloat1622float2(g2[k]), d = __bfloat1622float2(d2[k]);
+      const float sx = 1.f / (1.f + __expf(-g.x)), sy = 1.f / (1.f + __expf(-g.y));
+      oa2[k] = __floats2bfloat162_rn(d.x * g.x * sx, d.y * g.y * sy);
+      og2[k] = __floats2bfloat162_rn(d.x * a.x * sx * (1.f + g.x * (1.f - sx)), d.y * a.y * sy * (1.f + g.y * (1.f - sy)));
+    }
+    *reinterpret_cast<uint4 *>(dag + r * 2 * rd + 8 * j) = oa;
+    *reinterpret_cast<uint4 *>(dag + r * 2 * rd + rd + 8 * j) = og;
   }
 }
 
-// one warp per row (d <= 512: 16 values per lane); dgamma / dbeta accumulated per CTA in shared
-// memory, then one fp32 atomic per column per CTA
+// one warp per row, PER = ceil(d / 32) values per lane (a template parameter: the register arrays stay
+// small -- a runtime bound of 16 took 154 registers and 1/8 occupancy); a lane owns the same columns in
+// every row, so dgamma / dbeta accumulate in its registers; the CTA's 8 warps combine in shared memory at
+// the end, then one fp32 atomic per column per CTA
+template <int PER>
 __global__ void __launch_bounds__(256) k_ln_bwd(const float *__restrict__ y, const float *__restrict__ dXt,
                                                 const float *__restrict__ gamma, int d, int64_t rows, float eps,
                                                 bf16 *__restrict__ dy, float *__restrict__ dgam, float *__restrict__ dbet) {
-  extern __shared__ float acc[];  // [2][d]
-  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) acc[e] = 0.f;
-  __syncthreads();
+  extern __shared__ float acc[];  // [8 warps][2][d]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int per = (d + 31) / 32;
+  float ga[PER], ba[PER], gm[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    ga[k] = ba[k] = 0.f;
+    gm[k] = lane + 32 * k < d ? gamma[lane + 32 * k] : 0.f;
+  }
   for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < rows; r += (int64_t)gridDim.x * 8) {
-    float yv[16], gv[16];
+    float yv[PER], gv[PER], dv[PER];
     float s1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < per && lane + 32 * k < d) s1 += (yv[k] = y[r * d + lane + 32 * k]);
+    for (int k = 0; k < PER; ++k) {  // both rows' loads first (latency-bound kernel)
+      const bool in = lane + 32 * k < d;
+      yv[k] = in ? y[r * d + lane + 32 * k] : 0.f;
+      dv[k] = in ? dXt[r * d + lane + 32 * k] : 0.f;
+      s1 += yv[k];
+    }
     const float mu = warp_sum(s1) / d;
     float s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < per && lane + 32 * k < d) s2 += (yv[k] - mu) * (yv[k] - mu);
+    for (int k = 0; k < PER; ++k)
+      if (lane + 32 * k < d) s2 += (yv[k] - mu) * (yv[k] - mu);
     const float inv = rsqrtf(warp_sum(s2) / d + eps);
     float m1 = 0.f, m2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (k < per && lane + 32 * k < d) {
-        const int e = lane + 32 * k;
-        const float xh = (yv[k] - mu) * inv, g = dXt[r * d + e];
-        atomicAdd(&acc[e], g * xh);
-        atomicAdd(&acc[d + e], g);
-        gv[k] = g * gamma[e];
-        yv[k] = xh;
-        m1 += gv[k];
-        m2 += gv[k] * xh;
-      }
+    for (int k = 0; k < PER; ++k) {
+      const float xh = (yv[k] - mu) * inv, g = dv[k];
+      ga[k] += g * xh;
+      ba[k] += g;
+      gv[k] = g * gm[k];
+      yv[k] = xh;
+      m1 += gv[k];
+      m2 += gv[k] * xh;
     }
     m1 = warp_sum(m1) / d;
     m2 = warp_sum(m2) / d;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < per && lane + 32 * k < d) dy[r * d + lane + 32 * k] = __float2bfloat16_rn((gv[k] - m1 - yv[k] * m2) * inv);
+    for (int k = 0; k < PER; ++k)
+      if (lane + 32 * k < d) dy[r * d + lane + 32 * k] = __float2bfloat16_rn((gv[k] - m1 - yv[k] * m2) * inv);
   }
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if (lane + 32 * k < d) {
+      acc[(w * 2) * d + lane + 32 * k] = ga[k];
+      acc[(w * 2 + 1) * d + lane + 32 * k] = ba[k];
+    }
   __syncthreads();
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    atomicAdd(dgam + e, acc[e]);
-    atomicAdd(dbet + e, acc[d + e]);
+    float sg = 0.f, sb = 0.f;
+    for (int q = 0; q < 8; ++q) {
+      sg += acc[(q * 2) * d + e];
+      sb += acc[(q * 2 + 1) * d + e];
+    }
+    atomicAdd(dgam + e, sg);
+    atomicAdd(dbet + e, sb);
   }
 }
 
 // row-major C [m x n] (+)= A [m x k] . B [k x n] with optional transposes, all row-major storage,
-// bf16 operands, fp32 C, fp32 compute (cuBLAS is column-major: C^T = B^T A^T)
+// bf16 operands, C in bf16 or fp32, fp32 compute (cuBLAS is column-major: C^T = B^T A^T)
 cublasStatus_t gemm_rm(cublasHandle_t hb, bool ta, bool tb, int m, int n, int k, const void *A, int lda, const void *B,
-                       int ldb, float *C, int ldc, float beta) {
+                       int ldb, void *C, int ldc, float beta, bool c_bf16 = false) {
   const float alpha = 1.f;
   return cublasGemmEx(hb, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &alpha, B,
-                      CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
-                      CUBLAS_GEMM_DEFAULT);
+                      CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C, c_bf16 ? CUDA_R_16BF : CUDA_R_32F, ldc,
+                      CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
 }
 
 }  // namespace
 
-// Scratch is the caller's: a, g, dh fp32 [R x rd]; h, da, dg bf16 [R x rd]; y fp32 [R x d]; dy bf16 [R x d]
+// Scratch is the caller's: ag, dag bf16 [R x 2rd]; h, dh bf16 [R x rd]; y fp32 [R x d]; dy bf16 [R x d]
 size_t hist_bwd_scratch_bytes(int d, int rd, int64_t R) {
-  return (size_t)R * rd * (3 * 4 + 3 * 2) + (size_t)R * d * (4 + 2) + 4096;
+  return (size_t)R * rd * (4 * 2 + 2 * 2) + (size_t)R * d * (4 + 2) + 4096;
 }
 
-cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, const bf16 *Wu, const bf16 *Wv,
-                     const bf16 *Wo, const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv,
-                     float *dWo, float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st) {
+cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, const bf16 *W1, const bf16 *Wo,
+                     const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
+                     float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st) {
   if (!*blas) {
     cublasHandle_t hb;
     if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return cudaErrorInitializationError;
@@ -120,8 +173,8 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
     p += (bytes + 255) / 256 * 256;
     return q;
   };
-  float *a = (float *)take((size_t)R * rd * 4), *g = (float *)take((size_t)R * rd * 4), *dh = (float *)take((size_t)R * rd * 4);
-  bf16 *h = (bf16 *)take((size_t)R * rd * 2), *da = (bf16 *)take((size_t)R * rd * 2), *dg = (bf16 *)take((size_t)R * rd * 2);
+  bf16 *ag = (bf16 *)take((size_t)R * 2 * rd * 2), *dag = (bf16 *)take((size_t)R * 2 * rd * 2);
+  bf16 *h = (bf16 *)take((size_t)R * rd * 2), *dh = (bf16 *)take((size_t)R * rd * 2);
   float *y = (float *)take((size_t)R * d * 4);
   bf16 *dy = (bf16 *)take((size_t)R * d * 2);
   cudaError_t e;
@@ -134,27 +187,30 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
   for (int64_t r0 = 0; r0 < rows; r0 += R) {
     const int n = (int)std::min<int64_t>(R, rows - r0);
     const bf16 *Xb = X + r0 * d;
-    // recompute the forward: a = X Wu, g = X Wv, h = a silu(g) (bf16), y = h Wo
-    if (gemm_rm(hb, false, false, n, rd, d, Xb, d, Wu, rd, a, rd, 0.f) != CUBLAS_STATUS_SUCCESS ||
-        gemm_rm(hb, false, false, n, rd, d, Xb, d, Wv, rd, g, rd, 0.f) != CUBLAS_STATUS_SUCCESS)
+    // recompute the forward: [a | g] = X [Wu | Wv] (one GEMM, bf16), h = a silu(g) (bf16), y = h Wo (fp32)
+    if (gemm_rm(hb, false, false, n, 2 * rd, d, Xb, d, W1, 2 * rd, ag, 2 * rd, 0.f, true) != CUBLAS_STATUS_SUCCESS)
       return cudaErrorUnknown;
     note_launch(3);
-    k_swiglu_fwd<<<ew, 256, 0, st>>>(a, g, h, (int64_t)n * rd);
+    k_swiglu_fwd<<<4 * ew, 256, 0, st>>>(ag, h, rd, (int64_t)n);
     if (gemm_rm(hb, false, false, n, d, rd, h, rd, Wo, d, y, d, 0.f) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
     // LayerNorm backward -> dy (bf16), dgamma, dbeta
-    k_ln_bwd<<<std::min<int64_t>((n + 7) / 8, ew), 256, 2 * d * sizeof(float), st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy,
-                                                                                     dgam, dbet);
-    // dWo += H^T dy;  dH = dy Wo^T
+    {
+      const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * ew);
+      const size_t sm = 16 * d * sizeof(float);
+      if (d <= 128) k_ln_bwd<4><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
+      else if (d <= 256) k_ln_bwd<8><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
+      else k_ln_bwd<16><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
+    }
+    // dWo += H^T dy;  dH = dy Wo^T (bf16)
     if (gemm_rm(hb, true, false, rd, d, n, h, rd, dy, d, dWo, d, 1.f) != CUBLAS_STATUS_SUCCESS ||
-        gemm_rm(hb, false, true, n, rd, d, dy, d, Wo, d, dh, rd, 0.f) != CUBLAS_STATUS_SUCCESS)
+        gemm_rm(hb, false, true, n, rd, d, dy, d, Wo, d, dh, rd, 0.f, true) != CUBLAS_STATUS_SUCCESS)
       return cudaErrorUnknown;
-    k_swiglu_bwd<<<ew, 256, 0, st>>>(a, g, dh, da, dg, (int64_t)n * rd);
-    // dWu += X^T da, dWv += X^T dg;  dX = da Wu^T + dg Wv^T
+    k_swiglu_bwd<<<4 * ew, 256, 0, st>>>(ag, dh, dag, rd, (int64_t)n);
+    // dWu += X^T da, dWv += X^T dg;  dX += [da | dg] [Wu | Wv]^T (one GEMM, K = 2 rd)
     float *dXb = dX + r0 * d;
-    if (gemm_rm(hb, true, false, d, rd, n, Xb, d, da, rd, dWu, rd, 1.f) != CUBLAS_STATUS_SUCCESS ||
-        gemm_rm(hb, true, false, d, rd, n, Xb, d, dg, rd, dWv, rd, 1.f) != CUBLAS_STATUS_SUCCESS ||
-        gemm_rm(hb, false, true, n, d, rd, da, rd, Wu, rd, dXb, d, 1.f) != CUBLAS_STATUS_SUCCESS ||
-        gemm_rm(hb, false, true, n, d, rd, dg, rd, Wv, rd, dXb, d, 1.f) != CUBLAS_STATUS_SUCCESS)
+    if (gemm_rm(hb, true, false, d, rd, n, Xb, d, dag, 2 * rd, dWu, rd, 1.f) != CUBLAS_STATUS_SUCCESS ||
+        gemm_rm(hb, true, false, d, rd, n, Xb, d, dag + rd, 2 * rd, dWv, rd, 1.f) != CUBLAS_STATUS_SUCCESS ||
+        gemm_rm(hb, false, true, n, d, 2 * rd, dag, 2 * rd, W1, 2 * rd, dXb, d, 1.f) != CUBLAS_STATUS_SUCCESS)
       return cudaErrorUnknown;
   }
   return cudaGetLastError();
