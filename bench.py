@@ -183,6 +183,74 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def e2e_from_ids(model, wl, xth, K, st, world, total_targets):
+    """Pinned host ids -> H2D (non-blocking, on the stream) -> stca_encode_history -> project -> forward ->
+    D2H of Z and z, K pipelined steps, CUDA events on the stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2511_06077_b200 as stca
+    c = wl.cfg
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n_video, n_action, n_pos, n_td = 1 << 20, 16, max(c.L_infer or 0, int(wl.lengths.max())), 32
+    tab = lambda n: (torch.randn(n, c.d, device="cuda", generator=g) * 0.05).to(torch.bfloat16).view(torch.int16)
+    video, action, position, tdelta = tab(n_video + 1), tab(n_action + 1), tab(n_pos), tab(n_td)
+    rng = np.random.default_rng(12)
+    T, B = wl.T, len(wl.lengths)
+    vid = torch.from_numpy(rng.integers(0, n_video + n_video // 100, T)).pin_memory()  # ~1 % out of vocabulary
+    act = torch.from_numpy(rng.integers(0, n_action, T)).pin_memory()
+    req = torch.from_numpy(np.full(B, 1_700_000_000, dtype=np.int64)).pin_memory()
+    ts = torch.from_numpy(1_700_000_000 - rng.integers(0, 1 << 24, T)).pin_memory()
+    hoff = torch.from_numpy(np.asarray(wl.hist_off, dtype=np.int64)).pin_memory()
+    xtp = torch.from_numpy(np.ascontiguousarray(xth)).pin_memory()
+    Zp = torch.empty(wl.Nt, c.M, c.d).pin_memory()
+    zp = torch.empty(wl.Nt, c.d).pin_memory()
+    # ids travel on a copy stream into two device buffer sets, so step k + 1's upload overlaps step k
+    dvs = [[torch.empty_like(a, device="cuda") for a in (vid, act, ts, hoff, req)] for _ in range(2)]
+    X = torch.empty(T, c.d, dtype=torch.int16, device="cuda")
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    k_ = [0]
+
+    def step():
+        b_ = k_[0] & 1
+        k_[0] += 1
+        dv = dvs[b_]
+        cs.wait_event(ev_free[b_])  # encode of two steps ago has read this buffer set
+        with torch.cuda.stream(cs):
+            for a, b in zip((vid, act, ts, hoff, req), dv):
+                b.copy_(a, non_blocking=True)
+            ev_in[b_].record(cs)
+        st.wait_event(ev_in[b_])
+        stca.encode_history(video, action, position, dv[0], dv[1], dv[3], tdelta=tdelta, timestamp=dv[2],
+                            req_time=dv[4], X=X, stream=st)
+        ev_free[b_].record(st)
+        model.project_history(X, wl.hist_off, stream=st)
+        model.forward(xtp, wl.tgt_off, Zp, zp, stream=st, sync=False)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    device_align(world)
+    e0.record(st)
+    for _ in range(K):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / K], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    h2d = sum(a.numel() * a.element_size() for a in (vid, act, ts, hoff, req)) + xtp.numel() * xtp.element_size()
+    return {"value": total_targets / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(Zp.numel() * 4 + zp.numel() * 4),
+            "input": "raw history ids (video, action, timestamp: 24 B per row) + x_t; X encoded on the device "
+                     "(stca_encode_history: video 2^20 + OOV, action 16, position, log2-time-delta tables, bf16, "
+                     "resident) then projected",
+            "per": "rank 0's shard bytes; time = max over ranks" if world > 1 else "the whole step"}
+
+
 def device_align(world):
     """Aligns the ranks' STREAMS (not only their hosts) right before a timed region: a one-element
     all-reduce on the current stream completes on every device at about the same time, so host launch
@@ -405,6 +473,14 @@ def main():
                "d2h_bytes_per_step": int(Zp.numel() * 4 + zp.numel() * 4),
                "per": "rank 0's shard bytes; time = max over ranks" if world > 1 else "the whole step"}
 
+    # e2e from RAW IDS (NEXT-4): per step the host sends each history row's (video id, action id,
+    # timestamp) -- 24 bytes instead of the 2d-byte embedding row -- and the library's encoding prologue
+    # (stca_encode_history) builds X on the device from resident tables.  Same pipelined
+    # loop and timing as e2e; a secondary field (the values of X differ from the main workload's).
+    e2e_ids = None
+    if not args.no_e2e and bf16 and not split:
+        e2e_ids = e2e_from_ids(model, wl, xth, K, st, world, total_targets)
+
     if rank == 0:
         pk = peaks()
         clocks = clk.summary()
@@ -458,6 +534,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": e2e,
+            "e2e_ids": e2e_ids,
             "lib_sha256": lib_sha256()[:16],
         }
         if world == 1 and not args.no_oracle:

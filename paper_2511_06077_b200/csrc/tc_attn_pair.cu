@@ -53,7 +53,10 @@ struct PCfg {
   static constexpr int SS = D == 512 ? 2 : 4, PS = D == 512 ? 2 : 4;
   static constexpr int U_BYTES = NB * 8192;           // 64 rows x d: NB boxes of [64 x 64]
   static constexpr int P_BYTES = 64 * 64 * 2;         // [64 rows x 64 keys] bf16, SW128 K-major
-  static constexpr int SMEM = 1024 + SS * S_BYTES + PS * PV_BYTES + U_BYTES + 2 * P_BYTES + 6 * 128 * 4 + 2 * 64 * 4 + 256;
+  // S and P buffers: 3 each, so the leader issues S two tiles ahead of PV (S(j), then PV(j - 2)) and the
+  // softmax of a tile has two tiles of tensor work to hide behind
+  static constexpr int NSB = 3, LA = NSB - 1;
+  static constexpr int SMEM = 1024 + SS * S_BYTES + PS * PV_BYTES + U_BYTES + NSB * P_BYTES + 6 * 128 * 4 + 2 * 64 * 4 + 256;
   static constexpr uint32_t TO = 0, TS = 256;         // TMEM columns: O (NPV x 128) | S0 | S1 (32 each)
   static constexpr int THREADS = 352;  // warps 0-7 softmax (0-3) / output, 8 TMA (S parts), 9 MMA, 10 TMA (PV parts)
 };
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(352, 1)
   uint8_t *sXp = sXs + C::SS * C::S_BYTES;       // PV-part ring
   uint8_t *sU = sXp + C::PS * C::PV_BYTES;
   uint8_t *sP = sU + C::U_BYTES;
-  float *sXm = reinterpret_cast<float *>(sP + 2 * C::P_BYTES);  // [2 buf][2 col half][128 lane] tile maxima | [2][128] sums
+  float *sXm = reinterpret_cast<float *>(sP + C::NSB * C::P_BYTES);  // [2 buf][2 col half][128 lane] tile maxima | [2][128] sums
   float *sMl = sXm + 6 * 128;                                    // [2][64]: reference maximum, total sum per row
   uint64_t *bar = reinterpret_cast<uint64_t *>(sMl + 2 * 64);
   uint64_t *sfull = bar;                    // SS (leader: S-part TMA bytes of both CTAs)
@@ -77,12 +80,12 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t *pfull2 = sempty + C::SS;        // PS (leader: PV-part TMA bytes of both CTAs)
   uint64_t *pempty = pfull2 + C::PS;        // PS (commit multicast: PV of the slot's tile done)
   uint64_t *u_full = pempty + C::PS;        // 1 (leader: U bytes of both CTAs)
-  uint64_t *s_full = u_full + 1;            // 2 (commit multicast)
-  // (no "S buffer free" barrier: S(j + 2) is issued after PV(j), which waited for P(j), so the
-  // softmax has long read S(j))
-  uint64_t *p_full = s_full + 2;            // 2 (leader: one arrive per CTA once its P half is written)
-  uint64_t *pv_done = p_full + 2;           // 2 (commit multicast)
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(pv_done + 2);
+  uint64_t *s_full = u_full + 1;            // NSB (commit multicast)
+  // (no "S buffer free" barrier: S(j + NSB) is issued after PV(j + 1 - ...) -- after PV(j), which waited
+  // for P(j), so the softmax has long read S(j))
+  uint64_t *p_full = s_full + C::NSB;       // NSB (leader: one arrive per CTA once its P half is written)
+  uint64_t *pv_done = p_full + C::NSB;      // NSB (commit multicast)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(pv_done + C::NSB);
 
   const AttnItem it = items[blockIdx.x >> 1];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(352, 1)
       mbar_init(&pempty[s], 1);
     }
     mbar_init(u_full, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::NSB; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 2);
       mbar_init(&pv_done[b], 1);
@@ -174,8 +177,8 @@ __global__ void __launch_bounds__(352, 1)
       mbar_wait(u_full, 0);
       int s = 0, ph = 0, sp = 0, pph = 0;  // ring slots of S(j) and of PV(j - 1)
       auto issue_pv = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
+        const int b = j % C::NSB;
+        mbar_wait(&p_full[b], (j / C::NSB) & 1);
         mbar_wait(&pfull2[sp], pph);
         tc_fence_after();
         const uint32_t xs = aXp + sp * C::PV_BYTES, ps = aP + b * C::P_BYTES;
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(352, 1)
         if (++sp == C::PS) { sp = 0; pph ^= 1; }
       };
       for (int j = 0; j < nt; ++j) {
-        const int b = j & 1;
+        const int b = j % C::NSB;
         mbar_wait(&sfull[s], ph);
         tc_fence_after();
         const uint32_t xs = aXs + s * C::S_BYTES;
@@ -203,9 +206,9 @@ __global__ void __launch_bounds__(352, 1)
         umma_commit_pair_mc(&s_full[b], 0x3);
         umma_commit_pair_mc(&sempty[s], 0x3);
         if (++s == C::SS) { s = 0; ph ^= 1; }
-        if (j >= 1) issue_pv(j - 1);  // S(j) runs while the softmax of tile j - 1 finishes
+        if (j >= C::LA) issue_pv(j - C::LA);  // S(j) and S(j - 1) run while the softmax of tile j - LA finishes
       }
-      if (nt >= 1) issue_pv(nt - 1);
+      for (int j = nt > C::LA ? nt - C::LA : 0; j < nt; ++j) issue_pv(j);
     }
   } else {  // ---------------- warps 0-7: softmax and output ----------------
     // warp w: TMEM lane quarter q = w % 4, S column half ch = w / 4.  Thread: lane L = 32 q + lane holds
@@ -214,11 +217,13 @@ __global__ void __launch_bounds__(352, 1)
     const int q = warp & 3, ch = warp >> 2;
     const int L = q * 32 + lane, r = L & 63, hf = L >> 6;
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
-    const uint32_t pfull_b[2] = {mapa_shared(&p_full[0], 0), mapa_shared(&p_full[1], 0)};
+    uint32_t pfull_b[C::NSB];
+#pragma unroll
+    for (int i = 0; i < C::NSB; ++i) pfull_b[i] = mapa_shared(&p_full[i], 0);
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < nt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      const int b = j % C::NSB;
+      mbar_wait(&s_full[b], (j / C::NSB) & 1);
       tc_fence_after();
       uint32_t sr[16];
       tmem_ld16(tmem + lanes + C::TS + b * 32 + 16 * ch, sr);
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(352, 1)
       for (int c = 0; c < 16; ++c)
         if (c < kvalid) mx[c & 3] = fmaxf(mx[c & 3], __uint_as_float(sr[c]));
       float tm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-      float *xm = sXm + b * 256;
+      float *xm = sXm + (j & 1) * 256;  // two buffers suffice: every thread passes two barriers between uses
       xm[ch * 128 + L] = tm;
       named_bar_sync(1, 256);
       tm = fmaxf(fmaxf(tm, xm[(ch ^ 1) * 128 + L]), fmaxf(xm[ch * 128 + (L ^ 64)], xm[(ch ^ 1) * 128 + (L ^ 64)]));
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(352, 1)
       } else {
         const bool need = tm > m_ref + STCA_PAIR_LAZY;  // identical for the row's four threads
         if (__any_sync(0xffffffffu, need)) {  // rescale this lane's half of the O columns once the PVs so far are done
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&pv_done[(j - 1) % C::NSB], ((j - 1) / C::NSB) & 1);
           tc_fence_after();
           const float f = need ? ex2(m_ref - tm) : 1.f;
           if (need) {
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(352, 1)
           tmem_st_wait();
         }
       }
-      if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // PV of tile j - 2 has read P buffer b
+      if (j >= C::NSB) mbar_wait(&pv_done[b], ((j - C::NSB) / C::NSB) & 1);  // PV of tile j - NSB has read P buffer b
       uint32_t w[8];
       float lsum = 0.f;
 #pragma unroll
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(352, 1)
     // the row's total sum: its four partial sums
     float *sl = sXm + 4 * 128;
     sl[ch * 128 + L] = l;
-    if (nt >= 1) mbar_wait(&pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);  // the last PV
+    if (nt >= 1) mbar_wait(&pv_done[(nt - 1) % C::NSB], ((nt - 1) / C::NSB) & 1);  // the last PV
     tc_fence_before();
     named_bar_sync(1, 256);
     tc_fence_after();
