@@ -47,28 +47,30 @@ __global__ void k_swiglu_bwd32(float *__restrict__ a, float *__restrict__ g, con
   }
 }
 
-// one warp per row (d <= 512): out = LN(y) gamma + beta
+// one warp per row, PER = ceil(d / 32) values per lane (compile-time: small register arrays)
+template <int PER>
 __global__ void k_ln32(const float *__restrict__ y, const float *__restrict__ gam, const float *__restrict__ bet, int d,
                        int64_t rows, float eps, float *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    float v[16], s1 = 0.f;
+    float v[PER], s1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = lane + 32 * k < d ? y[r * d + lane + 32 * k] : 0.f, s1 += v[k];
+    for (int k = 0; k < PER; ++k) v[k] = lane + 32 * k < d ? y[r * d + lane + 32 * k] : 0.f, s1 += v[k];
     const float mu = warp_sum(s1) / d;
     float s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < PER; ++k)
       if (lane + 32 * k < d) s2 += (v[k] - mu) * (v[k] - mu);
     const float inv = rsqrtf(warp_sum(s2) / d + eps);
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < PER; ++k)
       if (lane + 32 * k < d) out[r * d + lane + 32 * k] = (v[k] - mu) * inv * gam[lane + 32 * k] + bet[lane + 32 * k];
   }
 }
 
 // LN backward, one warp per row, statistics recomputed from y; dy fp32; dgamma / dbeta per CTA in shared
 // memory, then one atomic per column per CTA
+template <int PER>
 __global__ void __launch_bounds__(256) k_ln_bwd32(const float *__restrict__ y, const float *__restrict__ dout,
                                                   const float *__restrict__ gam, int d, int64_t rows, float eps,
                                                   float *__restrict__ dy, float *__restrict__ dgam, float *__restrict__ dbet) {
@@ -77,18 +79,18 @@ __global__ void __launch_bounds__(256) k_ln_bwd32(const float *__restrict__ y, c
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < rows; r += (int64_t)gridDim.x * 8) {
-    float v[16], gv[16], s1 = 0.f;
+    float v[PER], gv[PER], s1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = lane + 32 * k < d ? y[r * d + lane + 32 * k] : 0.f, s1 += v[k];
+    for (int k = 0; k < PER; ++k) v[k] = lane + 32 * k < d ? y[r * d + lane + 32 * k] : 0.f, s1 += v[k];
     const float mu = warp_sum(s1) / d;
     float s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < PER; ++k)
       if (lane + 32 * k < d) s2 += (v[k] - mu) * (v[k] - mu);
     const float inv = rsqrtf(warp_sum(s2) / d + eps);
     float m1 = 0.f, m2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < PER; ++k) {
       if (lane + 32 * k < d) {
         const int e = lane + 32 * k;
         const float xh = (v[k] - mu) * inv, g = dout[r * d + e];
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd32(const float *__restrict__ y, c
     m1 = warp_sum(m1) / d;
     m2 = warp_sum(m2) / d;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < PER; ++k)
       if (lane + 32 * k < d) dy[r * d + lane + 32 * k] = (gv[k] - m1 - v[k] * m2) * inv;
   }
   __syncthreads();
@@ -206,7 +208,7 @@ cudaError_t stack_bwd(void **blas, const StackBwd &a, cudaStream_t st) {
   CK(cudaMemcpy2DAsync(oc + (size_t)M * d, ldo * 4, xt, (size_t)d * 4, (size_t)d * 4, Nt, cudaMemcpyDeviceToDevice, st));
   CK(ffn_fwd(xt, a.qWu[0], a.qWv[0], a.qWo[0], yq1));
   note_launch();
-  k_ln32<<<ew, 256, 0, st>>>(yq1, a.qg, a.qb, d, Nt, a.eps, q[0]);
+  k_ln32<4><<<ew, 256, 0, st>>>(yq1, a.qg, a.qb, d, Nt, a.eps, q[0]);  // d = 128 (stca_backward's path)
   for (int i = 1; i <= M; ++i) {
     CK(bf16_to_f32(a.Y[i - 1], Y, NQ * d, st));
     for (int r = 0; r < h; ++r)  // cat_r = Y_r W_V[:, C_r]
@@ -254,7 +256,7 @@ cudaError_t stack_bwd(void **blas, const StackBwd &a, cudaStream_t st) {
       SG(false, true, nt, d, d, 1.f, t, d, a.WC[L] + (size_t)L * d * d, d, 1.f, dO + (size_t)M * d, ldo);
     } else {  // Eq.(3): q1 = LN(FFN_Q1(x_t))
       note_launch();
-      k_ln_bwd32<<<lnb, 256, 2 * d * sizeof(float), st>>>(yq1, dq, a.qg, d, Nt, a.eps, t, a.g_qg, a.g_qb);
+      k_ln_bwd32<4><<<lnb, 256, 2 * d * sizeof(float), st>>>(yq1, dq, a.qg, d, Nt, a.eps, t, a.g_qg, a.g_qb);
       CK(ffn_bwd(xt, t, a.qWu[0], a.qWv[0], a.qWo[0], dq, a.g_qWu[0], a.g_qWv[0], a.g_qWo[0]));
       const float one = 1.f;
       if (cublasSgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, d, nt, &one, dO + (size_t)M * d, (int)ldo, &one, dq, d,
