@@ -285,13 +285,19 @@ def lib_sha256():
     return h.hexdigest()
 
 
+def src_sha256():
+    from paper_2511_06077_b200 import build as _b
+    return _b.source_digest()
+
+
 def ncu_for(config, kernel):
     """The committed ncu launch-list summary (profiles/ncu_r2.json, tools/ncu_summary.py) of `kernel` at
-    `config` -- only if that capture ran THIS library build (sha256), else None."""
+    `config` -- only if that capture ran a build of THESE sources (source digest, or the same binary),
+    else None."""
     tf = os.path.join(ROOT, "profiles", "ncu_r2.json")
     try:
         t = json.load(open(tf)).get(config, {})
-        if t.get("lib_sha256") == lib_sha256():
+        if t.get("src_sha256") == src_sha256() or t.get("lib_sha256") == lib_sha256():
             return dict(t.get(kernel, {}), source=t.get("source"))
     except Exception:
         pass
@@ -536,6 +542,7 @@ def main():
             "e2e": e2e,
             "e2e_ids": e2e_ids,
             "lib_sha256": lib_sha256()[:16],
+            "src_sha256": src_sha256()[:16],
         }
         if world == 1 and not args.no_oracle:
             line["cpu_baseline"] = oracle_sample(gwl)

@@ -29,6 +29,22 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
          "-I" + os.path.join(ROOT, "include")]
 
 
+def source_digest() -> str:
+    """sha256 over the library's sources, its header and the compile flags: identifies a BUILD by what it
+    was built from (nvcc output is not bit-reproducible, so the binary's own hash changes on a rebuild of
+    the same sources).  Profiles keyed by it stay valid across rebuilds."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + FLAGS[:-1]).encode())
+    for name in sorted(os.listdir(CSRC)):
+        h.update(name.encode())
+        with open(os.path.join(CSRC, name), "rb") as f:
+            h.update(f.read())
+    with open(os.path.join(ROOT, "include", "stca.h"), "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
 def _deps_mtime() -> float:
     m = os.path.getmtime(os.path.join(ROOT, "include", "stca.h"))
     for f in os.listdir(CSRC):

@@ -2,8 +2,8 @@
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv
         --log-file <csv> python bench.py --config <cfg> ...)
 into profiles/ncu_r2.json: per config, the projection and attention kernels' average cold-cache launch duration
-and DRAM bytes per launch, stamped with the sha256 of the library the capture ran (bench.py uses an entry only
-when it matches the loaded library).
+and DRAM bytes per launch, stamped with the sha256 of the library binary the capture ran and the digest of the sources it was
+built from (bench.py uses an entry when either matches: nvcc builds are not bit-reproducible).
 
     python tools/ncu_summary.py <config>=<csv> ... [--lib paper_2511_06077_b200/libstca.so]
 """
@@ -58,12 +58,18 @@ def main():
     ap.add_argument("pairs", nargs="+")
     ap.add_argument("--lib", default=os.path.join(ROOT, "paper_2511_06077_b200", "libstca.so"))
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_r2.json"))
+    ap.add_argument("--lib-sha", default=None, help="the binary's sha256 if the capture ran another build of the "
+                                                    "same sources")
     a = ap.parse_args()
     sha = hashlib.sha256(open(a.lib, "rb").read()).hexdigest()
+    sys.path.insert(0, ROOT)
+    from paper_2511_06077_b200 import build as _b  # noqa: E402
+    src = _b.source_digest()
     res = json.load(open(a.out)) if os.path.exists(a.out) else {}
     for p in a.pairs:
         cfg, path = p.split("=", 1)
-        res[cfg] = {"lib_sha256": sha, "source": os.path.relpath(path, ROOT), **summarise(path)}
+        res[cfg] = {"lib_sha256": sha if a.lib_sha is None else a.lib_sha, "src_sha256": src,
+                    "source": os.path.relpath(path, ROOT), **summarise(path)}
     json.dump(res, open(a.out, "w"), indent=1)
     json.dump(res, sys.stdout, indent=1)
 
