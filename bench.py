@@ -274,7 +274,8 @@ def config_dict(wl, args):
                             if c.name == "split1" else
                             f"one global request set, LPT-sharded over {args.gpus} GPU(s) (stca_plan_shards), "
                             "no collective on the data path"),
-            "l2": "inputs larger than L2 (X and the X~ cache exceed 126 MB); no flush", "seed": args.seed}
+            "l2": "inputs larger than L2 (X and the X~ cache exceed 126 MB); no flush", "seed": args.seed,
+            **({"attention_form": args.form} if args.form != "reordered" else {})}
 
 
 def lib_sha256():
@@ -344,6 +345,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the per-phase profiled pass")
     ap.add_argument("--chunk-keys", type=int, default=0, help="split-K chunk cap in keys (0: library default)")
+    ap.add_argument("--form", choices=("reordered", "standard"), default="reordered",
+                    help="attention form: the paper's reordered Eq.(13) (default) or the standard Eq.(12) with K/V "
+                         "per head materialised (NEXT-3 variant, A/B)")
     ap.add_argument("--split-exchange", choices=("peer", "nccl"), default="peer",
                     help="split1 on > 1 GPU: partials read in place over peer memory (stca_split_peer_*, default) "
                          "or all-gathered by NCCL through the exchange callback")
@@ -392,6 +396,8 @@ def main():
                       device=local, chunk_keys=1280 if split else args.chunk_keys,
                       split_rank=rank if split else 0, split_world=world if split else 1,
                       exchange=stca.nccl_exchange() if split and world > 1 and args.split_exchange == "nccl" else None)
+    if args.form != "reordered":
+        model.set_attention_form(args.form)
     if split and world > 1 and args.split_exchange == "peer":  # partials read in place over NVLink
         model.split_peer_setup(64 << 20)
     bf16 = c.dtype == "bf16"

@@ -381,6 +381,20 @@ stca_status stca_split_peer_attach(stca_handle *h, void *const *bases);
 stca_status stca_ipc_open(const void *ipc_handle, int32_t device, void **ptr_out);
 stca_status stca_ipc_close(void *ptr);
 
+/* ---- NEXT-3 (i): the STANDARD attention form as a variant (Eq.(12),
+ * P:L177-182, against the reordered Eq.(13)) ----
+ * STCA_FORM_REORDERED (default): u = q W_Q^r W_K^r^T, attention over X~ itself, o = sum_r (alpha_r X~) W_V^r W_O^r.
+ * STCA_FORM_STANDARD: per layer the history's K^r = X~ W_K^r and V^r = X~ W_V^r are materialised for
+ * every head ([K^r | V^r | 0] in a d-column block per head, one tcgen05 GEMM, T' x h d bf16 in HBM), the
+ * query is q W_Q^r, the attention runs per (request, head) on the transposed tcgen05 kernel, and
+ * o = sum_r (alpha_r V^r) W_O^r.  Same function (P8 of the oracle pins), different cost: the form the
+ * paper's reordering argument is measured against.  bf16 path, d = 128, at most 64 targets per request,
+ * no split-history; UNSUPPORTED otherwise (checked here or at the forward).  Takes effect for the next
+ * stca_forward; the first switch to STANDARD builds its weights (synchronous). */
+#define STCA_FORM_REORDERED 0
+#define STCA_FORM_STANDARD 1
+stca_status stca_set_attention_form(stca_handle *h, int32_t form);
+
 #ifdef __cplusplus
 }
 #endif

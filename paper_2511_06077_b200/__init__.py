@@ -157,6 +157,10 @@ class STCA:
             lib().stca_destroy(self._h)
             self._h = None
 
+    def set_attention_form(self, form: str) -> None:
+        """"reordered" (Eq.(13), default) or "standard" (Eq.(12): K/V per head materialised; NEXT-3 variant)."""
+        self._check(lib().stca_set_attention_form(self._h, {"reordered": 0, "standard": 1}[form]))
+
     # ---- split-history over peer memory (stca_split_peer_*) ----
     def split_peer_export(self, capacity_bytes: int = 64 << 20):
         """Allocates this rank's exchange buffer; returns (device address, 64-byte IPC handle)."""

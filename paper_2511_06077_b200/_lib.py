@@ -57,7 +57,8 @@ SYMBOLS = ["stca_create", "stca_project_history", "stca_forward", "stca_destroy"
            "stca_plan_split", "stca_plan_persistent", "stca_read_cache", "stca_rlb_allocate", "stca_rlb_compact",
            "stca_profile", "stca_profile_read", "stca_session_open", "stca_project_history_session",
            "stca_encode_history", "stca_attention_backward", "stca_history_backward", "stca_backward",
-           "stca_split_peer_export", "stca_split_peer_attach", "stca_ipc_open", "stca_ipc_close"]
+           "stca_split_peer_export", "stca_split_peer_attach", "stca_ipc_open", "stca_ipc_close",
+           "stca_set_attention_form"]
 
 
 def lib():
@@ -139,6 +140,8 @@ def lib():
         L.stca_ipc_open.restype = ctypes.c_int32
         L.stca_ipc_close.argtypes = [ctypes.c_void_p]
         L.stca_ipc_close.restype = ctypes.c_int32
+        L.stca_set_attention_form.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.stca_set_attention_form.restype = ctypes.c_int32
         L.stca_session_open.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.stca_session_open.restype = ctypes.c_int32
         L.stca_project_history_session.argtypes = [ctypes.c_void_p, _I64P, _I64P, ctypes.c_void_p, ctypes.c_int64,

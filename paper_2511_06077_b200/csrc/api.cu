@@ -183,6 +183,11 @@ struct stca_handle {
   uint64_t epoch = 0;         // one per layer of every split forward (identical on all ranks)
   std::vector<uint8_t *> peer_bases;  // host copy of the G buffers' addresses
   uint8_t peer_uuid[16] = {};         // this device's UUID (also at byte 1024 of the exported buffer)
+  // NEXT-3 (i): the standard attention form (stca_set_attention_form): per layer W_Q and [W_K | W_V]
+  // zero-padded to d columns per head, W_O rows per head at the V block, in the tcgen05 layout
+  int attn_form = 0;
+  stca::TcWeights std_q[STCA_MAX_LAYERS], std_kv[STCA_MAX_LAYERS];
+  DevBuf kvbuf;  // [T' x h d]: per history row and head [K^r | V^r | 0]
   DevBuf act, sbwd_scratch, dxt_buf, gsink, dxsink;
   // stca_debug_capture (stage-isolated tests): copy U and Y of one layer during the next forward
   int cap_layer = 0;
@@ -202,7 +207,7 @@ struct stca_handle {
 
 static DevBuf *const *all_bufs(stca_handle *h, int *n) {
   static thread_local DevBuf *v[32];
-  DevBuf *list[] = {&h->act, &h->sbwd_scratch, &h->dxt_buf, &h->gsink, &h->dxsink,
+  DevBuf *list[] = {&h->act, &h->sbwd_scratch, &h->dxt_buf, &h->gsink, &h->dxsink, &h->kvbuf,
                     &h->xt_cache, &h->xin[0], &h->xin[1], &h->bwd_scratch, &h->xgather, &h->seg,    &h->proj_h, &h->proj_y, &h->xtin,
                     &h->ocat,     &h->q,    &h->c,       &h->hbuf,   &h->ybuf32, &h->U,      &h->Y,
                     &h->part,     &h->partg, &h->plan,   &h->zout,   &h->Zout};
@@ -1345,6 +1350,32 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     a.pad = 0;
     a.part_row = part_base[b] < 0 ? -1 : part_base[b] + o[5] * (tgt_off[b + 1] - tgt_off[b]) * hh + (o[1] - tgt_off[b] * hh);
   }
+  const bool stdf = h->attn_form == STCA_FORM_STANDARD;
+  if (stdf) {  // standard form: one item per (request, head) over the request's K^r / V^r, all on the narrow kernel
+    if (G > 1) return fail(h, STCA_ERR_UNSUPPORTED, "the standard attention form has no split-history mode");
+    items.clear();
+    items_nar.clear();
+    mi.clear();
+    part_rows = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t mb = tgt_off[b + 1] - tgt_off[b];
+      if (mb == 0) continue;
+      if (mb > 64)
+        return fail(h, STCA_ERR_UNSUPPORTED, "the standard attention form takes <= 64 targets per request (request %lld "
+                    "has %lld)", (long long)b, (long long)mb);
+      for (int r = 0; r < hh; ++r) {
+        stca::AttnItem a{};
+        a.qrow0 = tgt_off[b];
+        a.nq = (int32_t)mb;
+        a.key0 = h->coff[b];
+        a.klen = (int32_t)h->len[b];
+        a.chunk = 0;
+        a.pad = r;
+        a.part_row = -1;
+        items_nar.push_back(a);
+      }
+    }
+  }
   const int64_t nit_reg = (int64_t)items.size(), nit_nar = (int64_t)items_nar.size();
   items.insert(items.end(), items_nar.begin(), items_nar.end());  // [128-row kernel items | narrow items]
   nit = (int64_t)items.size();
@@ -1403,6 +1434,8 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
 #else
   const bool chain = h->bf16 && stca::tc_chain_supported(d, hh, h->cfg.r * d);
 #endif
+  if (stdf && !chain) return fail(h, STCA_ERR_UNSUPPORTED, "the standard attention form runs with the fused target side");
+  if (stdf) CU(h->kvbuf.ensure((size_t)std::max<int64_t>(h->T2, 1) * hh * d * es, st));
   auto chain_base = [&](int mode) {
     stca::TcChain c;
     c.mode = mode;
@@ -1421,7 +1454,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     stca::TcChain c = chain_base(0);
     c.W1t = L1.tc.W1q;
     c.Wot = L1.tc.Woq;
-    c.WQKt = L1.tc.WQK;
+    c.WQKt = stdf ? h->std_q[0].WQK : L1.tc.WQK;
     c.g = L1.gq;
     c.b = L1.bq;
     cudaEvent_t pa = h->prof_target ? prof_begin(h, st) : nullptr;
@@ -1448,7 +1481,16 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     }
     cudaEvent_t pa = prof_begin(h, st);
     for (int rep = 0; rep < h->reps_attn; ++rep) {  // idempotent (STCA_PROF_TWICE_ATTENTION)
-    if (tc_attn) {
+    if (stdf) {  // standard form, Eq.(12): [K^r | V^r | 0] = X~ [W_K^r | W_V^r | 0] for every head, then attention
+      if (rep == 0) {
+        cudaEvent_t pk = h->prof_target ? prof_begin(h, st) : nullptr;
+        CU(stca::tc_gemm(Xt, d, h->std_kv[i - 1].WQK, h->T2, hh * d, d, h->kvbuf.p, (int64_t)hh * d, nullptr, 0, st));
+        prof_end(h, STCA_PH_TARGET, pk, st);
+      }
+      if (nit_nar > 0)
+        CU(stca::tc_attention_narrow(h->U.p, NQ, h->kvbuf.p, h->T2, d_items + nit_reg, d_ctal + nar_at,
+                                     d_ctal + nar_at + n_ctas_nar + 1, n_ctas_nar, h->Y.p, part_i, st, hh));
+    } else if (tc_attn) {
       if (nit_nar > 0)
         CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, d_items + nit_reg,
                                      d_ctal + nar_at, d_ctal + nar_at + n_ctas_nar + 1,
@@ -1513,14 +1555,14 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       c.ocat_out = (uint8_t *)h->ocat.p + (size_t)i * d * es;
       c.Z = Zd + (size_t)(i - 1) * d;
       c.ldz = (int64_t)M * d;
-      c.WVOt = Ly.tc.WVO;
+      c.WVOt = stdf ? h->std_q[i - 1].WVO : Ly.tc.WVO;
       if (i < M) {
         LayerW &Ln = h->L[i];
         c.kc = i + 1;
         c.WCt = Ln.tc.WC;
         c.W1t = Ln.tc.W1q;
         c.Wot = Ln.tc.Woq;
-        c.WQKt = Ln.tc.WQK;
+        c.WQKt = stdf ? h->std_q[i].WQK : Ln.tc.WQK;
       } else if (zd) {
         c.kc = M + 1;
         c.WCt = h->tcz.WC;
@@ -1958,5 +2000,53 @@ extern "C" stca_status stca_ipc_close(void *ptr) {
     cudaGetLastError();
     return STCA_ERR_CUDA;
   }
+  return STCA_OK;
+}
+
+// ===========================================================================
+// NEXT-3 (i): the standard attention form, Eq.(12), as a measured variant
+// ===========================================================================
+extern "C" stca_status stca_set_attention_form(stca_handle *h, int32_t form) {
+  if (!h) return STCA_ERR_INVALID_ARG;
+  if (form != STCA_FORM_REORDERED && form != STCA_FORM_STANDARD) return fail(h, STCA_ERR_INVALID_ARG, "bad form %d", form);
+  if (form == STCA_FORM_REORDERED) {
+    h->attn_form = form;
+    return STCA_OK;
+  }
+  const int d = h->cfg.d, hh = h->cfg.h, M = h->cfg.M, dh = d / hh;
+  if (!h->bf16 || d != 128)
+    return fail(h, STCA_ERR_UNSUPPORTED, "the standard attention form runs on the bf16 path with d = 128 (d=%d)", d);
+  CU(cudaSetDevice(h->cfg.device));
+  CU(cudaDeviceSynchronize());
+  const float c = (float)(1.4426950408889634 / sqrt((double)dh));  // log2(e)/sqrt(d_h): scores in the log2 domain
+  std::vector<float> wq((size_t)d * d), wk((size_t)d * d), wv((size_t)d * d), wo((size_t)d * d);
+  for (int i = 1; i <= M; ++i) {
+    const std::string p = "L" + std::to_string(i) + ".";
+    if (!h->std_q[i - 1].WQK) {
+      CU(cudaMemcpy(wq.data(), h->w32[p + "WQ"], wq.size() * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(wk.data(), h->w32[p + "WK"], wk.size() * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(wv.data(), h->w32[p + "WV"], wv.size() * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(wo.data(), h->w32[p + "WO"], wo.size() * 4, cudaMemcpyDeviceToHost));
+      // per head r a d-column block: Q: [c W_Q^r | 0], KV: [W_K^r | W_V^r | 0]; O: rows of the V block = W_O^r
+      std::vector<float> q((size_t)d * hh * d, 0.f), kv((size_t)d * hh * d, 0.f), o((size_t)hh * d * d, 0.f);
+      for (int e = 0; e < d; ++e)
+        for (int r = 0; r < hh; ++r)
+          for (int cc = 0; cc < dh; ++cc) {
+            q[(size_t)e * hh * d + r * d + cc] = c * wq[(size_t)e * d + r * dh + cc];
+            kv[(size_t)e * hh * d + r * d + cc] = wk[(size_t)e * d + r * dh + cc];
+            kv[(size_t)e * hh * d + r * d + dh + cc] = wv[(size_t)e * d + r * dh + cc];
+          }
+      for (int r = 0; r < hh; ++r)
+        for (int cc = 0; cc < dh; ++cc)
+          memcpy(&o[((size_t)r * d + dh + cc) * d], &wo[(size_t)(r * dh + cc) * d], sizeof(float) * d);
+      void *qd = upload(h, q.data(), q.size()), *kvd = upload(h, kv.data(), kv.size()), *od = upload(h, o.data(), o.size());
+      if (!qd || !kvd || !od) return fail(h, STCA_ERR_OOM, "standard-form weight upload failed");
+      if (!stca::tc_prepare_layer(qd, od, nullptr, i, d, hh, &h->std_q[i - 1], [&](size_t n) { return dalloc(h, n); }) ||
+          !stca::tc_prepare_layer(kvd, nullptr, nullptr, i, d, hh, &h->std_kv[i - 1], [&](size_t n) { return dalloc(h, n); }))
+        return fail(h, STCA_ERR_OOM, "standard-form weight repack failed");
+    }
+  }
+  CU(cudaDeviceSynchronize());
+  h->attn_form = form;
   return STCA_OK;
 }

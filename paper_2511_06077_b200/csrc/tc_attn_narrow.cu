@@ -81,7 +81,12 @@ __device__ __forceinline__ float xreduce16(float (&v)[16], int lane) {
 __global__ void __launch_bounds__(NCfg::THREADS, 1)
     k_tc_attention_narrow(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapU,
                           const AttnItem *__restrict__ items, const int32_t *__restrict__ cta_off,
-                          const int32_t *__restrict__ cta_items, bf16 *__restrict__ Y, float *__restrict__ part) {
+                          const int32_t *__restrict__ cta_items, bf16 *__restrict__ Y, float *__restrict__ part,
+                          int yh) {
+  // yh = 1: the reordered form -- an item's U rows and keys are whole rows of U [N_t h x d] and X~.
+  // yh = h: the STANDARD form (Eq.(12), stca_set_attention_form): U [N_t x h d] holds per head r the query
+  // q W_Q^r (zero-padded to d columns) and the keys are K/V rows [T' x h d] holding [K^r | V^r | 0] per
+  // head; item.pad = r selects the 128-column block of both, and the output row of query t is t h + r.
   using C = NCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -135,24 +140,26 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
     if (lane == 0) {  // ---------------- TMA producer: per item U, then its key tiles ----------------
       int s = 0, ph = 0;
       // L2 prefetch cursor, STCA_NARROW_PF key tiles ahead of the loads, across item boundaries
-      int pf_n = i0, pf_j = 0, pf_nt = 0;
+      int pf_n = i0, pf_j = 0, pf_nt = 0, pf_col = 0;
       int64_t pf_key0 = 0;
       if (i0 < i1) {
         const AttnItem f = items[cta_items[i0]];
         pf_nt = (f.klen + C::BK - 1) / C::BK;
         pf_key0 = f.key0;
+        pf_col = C::D * f.pad;
       }
       auto pf_step = [&]() {  // prefetch the tile under the cursor, then advance it
         if (pf_n >= i1) return;
         const int32_t row = (int32_t)(pf_key0 + (int64_t)pf_j * C::BK);
-        tma_prefetch_l2(&mapX, 0, row);
-        tma_prefetch_l2(&mapX, 64, row);
+        tma_prefetch_l2(&mapX, pf_col, row);
+        tma_prefetch_l2(&mapX, pf_col + 64, row);
         if (++pf_j >= pf_nt) {
           pf_j = 0;
           if (++pf_n < i1) {
             const AttnItem f = items[cta_items[pf_n]];
             pf_nt = (f.klen + C::BK - 1) / C::BK;
             pf_key0 = f.key0;
+            pf_col = C::D * f.pad;
           }
         }
       };
@@ -164,16 +171,17 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         if (ni >= 2) mbar_wait(&u_free[ub], ((ni - 2) >> 1) & 1);
         mbar_expect_tx(&u_full[ub], C::U_BYTES);
         uint8_t *ud = sU + ub * C::U_BYTES;
-        tma_load_2d(ud, &mapU, &u_full[ub], 0, (int32_t)it.qrow0);  // rows past nq: finite, unused columns
-        tma_load_2d(ud + C::U_BYTES / 2, &mapU, &u_full[ub], 64, (int32_t)it.qrow0);
+        const int32_t col0 = C::D * it.pad;  // head block (standard form), 0 otherwise
+        tma_load_2d(ud, &mapU, &u_full[ub], col0, (int32_t)it.qrow0);  // rows past nq: finite, unused columns
+        tma_load_2d(ud + C::U_BYTES / 2, &mapU, &u_full[ub], col0 + 64, (int32_t)it.qrow0);
         for (int j = 0; j < nt; ++j) {
           if (STCA_NARROW_PF > 0) pf_step();
           mbar_wait(&x_empty[s], ph ^ 1);
           uint8_t *dst = sX + s * C::X_BYTES;
           const int32_t row = (int32_t)(it.key0 + (int64_t)j * C::BK);
           mbar_expect_tx(&x_full[s], C::X_BYTES);
-          tma_load_2d(dst, &mapX, &x_full[s], 0, row);
-          tma_load_2d(dst + C::X_BYTES / 2, &mapX, &x_full[s], 64, row);
+          tma_load_2d(dst, &mapX, &x_full[s], col0, row);
+          tma_load_2d(dst + C::X_BYTES / 2, &mapX, &x_full[s], col0 + 64, row);
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
                            sRed[(cg * 4 + 3) * 16 + e];
           const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
           if (it.part_row < 0) {
-            Y[(it.qrow0 + qn) * C::D + d] = y;
+            Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
           } else {  // partials hold the chunk's normalised output O / l, then (m, l)
             uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
             reinterpret_cast<bf16 *>(pr)[d] = y;
@@ -365,17 +373,19 @@ bool tc_attention_narrow_supported(int d, int max_rows) { return d == 128 && max
 
 cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                                 const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
-                                cudaStream_t st) {
+                                cudaStream_t st, int yh) {
   using C = tc::NCfg;
   if (n_ctas <= 0) return cudaSuccess;
   CUtensorMap mx, mu;
-  if (!tc::make_map_bf16(&mx, Xt, T2, C::D, C::D, C::BK) || !tc::make_map_bf16(&mu, U, NQ, C::D, C::D, C::NQ))
+  // standard form (yh = h): U is [N_t x h d], the keys [T' x h d]; an item reads one d-column block of each
+  const int64_t cols = (int64_t)C::D * yh;
+  if (!tc::make_map_bf16(&mx, Xt, T2, cols, cols, C::BK) || !tc::make_map_bf16(&mu, U, NQ / yh, cols, cols, C::NQ))
     return cudaErrorInvalidValue;
   cudaError_t e0 = smem_optin((const void *)tc::k_tc_attention_narrow, C::SMEM);
   if (e0 != cudaSuccess) return e0;
   note_launch();
   return launch_pdl(tc::k_tc_attention_narrow, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx, mu,
-                    items, cta_off, cta_items, (bf16 *)Y, part);
+                    items, cta_off, cta_items, (bf16 *)Y, part, yh);
 }
 
 }  // namespace stca

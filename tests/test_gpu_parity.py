@@ -270,3 +270,38 @@ def test_capacity_shape_d512_sampled():
     wl = workload.make_workload(cfg, seed=2, B=4, lengths=np.array([10000, 64, 1500, 4104]))
     Z, z = run_gpu(wl)
     check(wl, Z, z, TOL["bf16"])
+
+
+@pytest.mark.parametrize("lengths,m", [([300, 1, 4000, 129], 16), ([10000, 2500], 64)])
+def test_standard_form_variant(lengths, m):
+    """NEXT-3 (i): the standard attention form (Eq.(12): K^r, V^r materialised per head; stca_set_attention_form)
+    computes the same function as the reordered form (oracle pin P8) -- against the oracle within the bf16
+    tolerance, ragged lengths incl. L = 1 and a 10k history, up to 64 targets per request."""
+    import paper_2511_06077_b200 as stca
+    cfg = make_cfg(B=len(lengths), m=m, M=3)
+    wl = workload.make_workload(cfg, seed=21, lengths=np.asarray(lengths))
+    c = wl.cfg
+    mdl = stca.STCA(workload.full_weights(wl), d=c.d, h=c.h, r=c.r, M=c.M, dtype="bf16")
+    mdl.set_attention_form("standard")
+    Z, z = run_gpu(wl, model=mdl)
+    Zr, zr, _ = oracle.forward_workload(wl, nthreads=8)
+    assert rowrel(Z, Zr).max() <= 2e-2 and rowrel(z, zr).max() <= 2e-2
+    mdl.set_attention_form("reordered")  # back to the default form, same handle
+    Z2, _ = run_gpu(wl, model=mdl)
+    assert rowrel(Z2, Zr).max() <= 2e-2
+
+
+def test_standard_form_refusals():
+    import paper_2511_06077_b200 as stca
+    cfg = make_cfg(B=1, m=65, M=2)  # 65 targets: more than one transposed query tile
+    wl = workload.make_workload(cfg, seed=22, lengths=np.asarray([50]))
+    c = wl.cfg
+    mdl = stca.STCA(workload.full_weights(wl), d=c.d, h=c.h, r=c.r, M=c.M, dtype="bf16")
+    mdl.set_attention_form("standard")
+    with pytest.raises(stca.StcaError):
+        run_gpu(wl, model=mdl)
+    wide = workload.make_workload(make_cfg(B=1, m=2, d=256, h=4, M=2), seed=23, lengths=np.asarray([40]))
+    cw = wide.cfg
+    m2 = stca.STCA(workload.full_weights(wide), d=cw.d, h=cw.h, r=cw.r, M=cw.M, dtype="bf16")
+    with pytest.raises(stca.StcaError):  # d != 128
+        m2.set_attention_form("standard")
