@@ -78,6 +78,7 @@ __device__ __forceinline__ float xreduce16(float (&v)[16], int lane) {
 // the X~ ring, the S / P double buffers and their barriers run across items, U (by TMA) and O^T are
 // double-buffered per item, so the next item's first tiles load and multiply while this item's
 // sums are reduced and its outputs written.
+template <bool STD>
 __global__ void __launch_bounds__(NCfg::THREADS, 1)
     k_tc_attention_narrow(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapU,
                           const AttnItem *__restrict__ items, const int32_t *__restrict__ cta_off,
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         const AttnItem f = items[cta_items[i0]];
         pf_nt = (f.klen + C::BK - 1) / C::BK;
         pf_key0 = f.key0;
-        pf_col = C::D * f.pad;
+        pf_col = STD ? C::D * f.pad : 0;
       }
       auto pf_step = [&]() {  // prefetch the tile under the cursor, then advance it
         if (pf_n >= i1) return;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
             const AttnItem f = items[cta_items[pf_n]];
             pf_nt = (f.klen + C::BK - 1) / C::BK;
             pf_key0 = f.key0;
-            pf_col = C::D * f.pad;
+            pf_col = STD ? C::D * f.pad : 0;
           }
         }
       };
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         if (ni >= 2) mbar_wait(&u_free[ub], ((ni - 2) >> 1) & 1);
         mbar_expect_tx(&u_full[ub], C::U_BYTES);
         uint8_t *ud = sU + ub * C::U_BYTES;
-        const int32_t col0 = C::D * it.pad;  // head block (standard form), 0 otherwise
+        const int32_t col0 = STD ? C::D * it.pad : 0;  // head block (standard form)
         tma_load_2d(ud, &mapU, &u_full[ub], col0, (int32_t)it.qrow0);  // rows past nq: finite, unused columns
         tma_load_2d(ud + C::U_BYTES / 2, &mapU, &u_full[ub], col0 + 64, (int32_t)it.qrow0);
         for (int j = 0; j < nt; ++j) {
@@ -352,7 +353,8 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
                            sRed[(cg * 4 + 3) * 16 + e];
           const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
           if (it.part_row < 0) {
-            Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
+            if constexpr (STD) Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
+            else Y[(it.qrow0 + qn) * C::D + d] = y;
           } else {  // partials hold the chunk's normalised output O / l, then (m, l)
             uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
             reinterpret_cast<bf16 *>(pr)[d] = y;
@@ -381,11 +383,17 @@ cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64
   const int64_t cols = (int64_t)C::D * yh;
   if (!tc::make_map_bf16(&mx, Xt, T2, cols, cols, C::BK) || !tc::make_map_bf16(&mu, U, NQ / yh, cols, cols, C::NQ))
     return cudaErrorInvalidValue;
-  cudaError_t e0 = smem_optin((const void *)tc::k_tc_attention_narrow, C::SMEM);
+  // two instantiations: the standard form's per-item head offsets cost the reordered form registers
+  // (spill loads 60 -> 316 bytes, +12-18 % at multi / train) when compiled into one kernel
+  const void *kfn = yh > 1 ? (const void *)tc::k_tc_attention_narrow<true> : (const void *)tc::k_tc_attention_narrow<false>;
+  cudaError_t e0 = smem_optin(kfn, C::SMEM);
   if (e0 != cudaSuccess) return e0;
   note_launch();
-  return launch_pdl(tc::k_tc_attention_narrow, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx, mu,
-                    items, cta_off, cta_items, (bf16 *)Y, part, yh);
+  if (yh > 1)
+    return launch_pdl(tc::k_tc_attention_narrow<true>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx,
+                      mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
+  return launch_pdl(tc::k_tc_attention_narrow<false>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx,
+                    mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
 }
 
 }  // namespace stca
