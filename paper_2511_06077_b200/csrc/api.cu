@@ -1307,6 +1307,9 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
   // the others and launched separately), so a request's arithmetic never depends on its batch
   // (RLB invariance, P10).  STCA_NO_NARROW=1 disables it (A/B runs).
   static const bool no_narrow = getenv("STCA_NO_NARROW") && atoi(getenv("STCA_NO_NARROW")) != 0;
+  // a request with m_b h <= 32 takes the 32-column instantiation (also per request); STCA_NO_NARROW32=1
+  // sends it to the 64-column one (A/B runs)
+  static const bool no_narrow32 = getenv("STCA_NO_NARROW32") && atoi(getenv("STCA_NO_NARROW32")) != 0;
   const bool tc_narrow = tc_attn && !no_narrow;
   const int qtile = tc_attn ? 128 : tc_wide ? wide_qtile : 16;
   std::vector<int64_t> it6;
@@ -1328,7 +1331,7 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     max_rows = std::max<int>(max_rows, (int)rows);
     max_chunks = std::max<int>(max_chunks, (int)nc);
   }
-  std::vector<stca::AttnItem> items, items_nar;
+  std::vector<stca::AttnItem> items, items_nar[2];  // narrow: [0] 64 query columns, [1] 32
   items.reserve((size_t)nit);
   for (int64_t i = 0; i < nit; ++i) {
     const int64_t *o = &it6[6 * i];
@@ -1337,9 +1340,9 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
       const int32_t nc = stca_plan_chunks(h->len[b], (int32_t)h->chunk_cap, nullptr);
       if ((o[5] * G) / nc != grank) continue;
     }
-    const bool nar = tc_narrow && stca::tc_attention_narrow_supported(d, (int)std::min<int64_t>(
-                                                                        (tgt_off[b + 1] - tgt_off[b]) * hh, 1 << 30));
-    std::vector<stca::AttnItem> &dst = nar ? items_nar : items;
+    const int64_t brows = (tgt_off[b + 1] - tgt_off[b]) * hh;
+    const bool nar = tc_narrow && stca::tc_attention_narrow_supported(d, (int)std::min<int64_t>(brows, 1 << 30));
+    std::vector<stca::AttnItem> &dst = nar ? items_nar[brows <= 32 && !no_narrow32] : items;
     dst.emplace_back();
     stca::AttnItem &a = dst.back();
     a.qrow0 = o[1];
@@ -1354,7 +1357,8 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
   if (stdf) {  // standard form: one item per (request, head) over the request's K^r / V^r, all on the narrow kernel
     if (G > 1) return fail(h, STCA_ERR_UNSUPPORTED, "the standard attention form has no split-history mode");
     items.clear();
-    items_nar.clear();
+    items_nar[0].clear();
+    items_nar[1].clear();
     mi.clear();
     part_rows = 0;
     for (int64_t b = 0; b < B; ++b) {
@@ -1372,12 +1376,15 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
         a.chunk = 0;
         a.pad = r;
         a.part_row = -1;
-        items_nar.push_back(a);
+        items_nar[mb <= 32 && !no_narrow32].push_back(a);
       }
     }
   }
-  const int64_t nit_reg = (int64_t)items.size(), nit_nar = (int64_t)items_nar.size();
-  items.insert(items.end(), items_nar.begin(), items_nar.end());  // [128-row kernel items | narrow items]
+  const int64_t nit_reg = (int64_t)items.size();
+  const int64_t nit_nar[2] = {(int64_t)items_nar[0].size(), (int64_t)items_nar[1].size()};
+  const int64_t nar_first[2] = {nit_reg, nit_reg + nit_nar[0]};
+  // [128-row kernel items | narrow 64-column items | narrow 32-column items]
+  for (int k = 0; k < 2; ++k) items.insert(items.end(), items_nar[k].begin(), items_nar[k].end());
   nit = (int64_t)items.size();
   // persistent d = 128 attention: LPT bins of work items over the SMs (cost = key tiles + 2 for the
   // item's prologue / epilogue), CTA c runs cta_items[cta_off[c] .. cta_off[c+1]) in LPT order
@@ -1391,14 +1398,16 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
     stca_plan_persistent(cost.data(), nit_reg, n_ctas, ctal_resize(ctal, n_ctas, nit_reg), bin.data());
   }
   // persistent narrow attention: its own LPT lists appended to ctal (indices relative to its items)
-  int n_ctas_nar = 0;
-  const size_t nar_at = ctal.size();
-  if (nit_nar > 0) {
-    n_ctas_nar = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit_nar);
-    std::vector<int64_t> cost((size_t)nit_nar);
-    for (int64_t i = 0; i < nit_nar; ++i) cost[i] = (items[nit_reg + i].klen + 127) / 128 + 2;
-    std::vector<int32_t> bin((size_t)nit_nar), v;
-    stca_plan_persistent(cost.data(), nit_nar, n_ctas_nar, ctal_resize(v, n_ctas_nar, nit_nar), bin.data());
+  int n_ctas_nar[2] = {0, 0};
+  size_t nar_at[2] = {0, 0};
+  for (int k = 0; k < 2; ++k) {
+    nar_at[k] = ctal.size();
+    if (nit_nar[k] == 0) continue;
+    n_ctas_nar[k] = (int)std::min<int64_t>(stca::tc_attention_ctas(), nit_nar[k]);
+    std::vector<int64_t> cost((size_t)nit_nar[k]);
+    for (int64_t i = 0; i < nit_nar[k]; ++i) cost[i] = (items[nar_first[k] + i].klen + 127) / 128 + 2;
+    std::vector<int32_t> bin((size_t)nit_nar[k]), v;
+    stca_plan_persistent(cost.data(), nit_nar[k], n_ctas_nar[k], ctal_resize(v, n_ctas_nar[k], nit_nar[k]), bin.data());
     ctal.insert(ctal.end(), v.begin(), v.end());
   }
   // the plan [items | merge items | CTA lists], 256-byte aligned sections, in one upload
@@ -1487,14 +1496,17 @@ static stca_status forward_body(stca_handle *h, const void *xt, int64_t Nt, cons
         CU(stca::tc_gemm(Xt, d, h->std_kv[i - 1].WQK, h->T2, hh * d, d, h->kvbuf.p, (int64_t)hh * d, nullptr, 0, st));
         prof_end(h, STCA_PH_TARGET, pk, st);
       }
-      if (nit_nar > 0)
-        CU(stca::tc_attention_narrow(h->U.p, NQ, h->kvbuf.p, h->T2, d_items + nit_reg, d_ctal + nar_at,
-                                     d_ctal + nar_at + n_ctas_nar + 1, n_ctas_nar, h->Y.p, part_i, st, hh));
+      for (int k = 0; k < 2; ++k)
+        if (nit_nar[k] > 0)
+          CU(stca::tc_attention_narrow(h->U.p, NQ, h->kvbuf.p, h->T2, d_items + nar_first[k], d_ctal + nar_at[k],
+                                       d_ctal + nar_at[k] + n_ctas_nar[k] + 1, n_ctas_nar[k], h->Y.p, part_i, st, hh,
+                                       k ? 32 : 64));
     } else if (tc_attn) {
-      if (nit_nar > 0)
-        CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, d_items + nit_reg,
-                                     d_ctal + nar_at, d_ctal + nar_at + n_ctas_nar + 1,
-                                     n_ctas_nar, h->Y.p, part_i, st));
+      for (int k = 0; k < 2; ++k)
+        if (nit_nar[k] > 0)
+          CU(stca::tc_attention_narrow(h->U.p, NQ, Xt, h->T2, d_items + nar_first[k], d_ctal + nar_at[k],
+                                       d_ctal + nar_at[k] + n_ctas_nar[k] + 1, n_ctas_nar[k], h->Y.p, part_i, st, 1,
+                                       k ? 32 : 64));
       if (nit_reg > 0)
         CU(stca::tc_attention(h->U.p, NQ, Xt, h->T2, d_items, d_ctal,
                             d_ctal + n_ctas + 1, n_ctas, d, h->Y.p, part_i, st));

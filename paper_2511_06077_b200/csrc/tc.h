@@ -66,10 +66,11 @@ cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N
 // d in {256, 512}: 64-row query tiles, M = 64 MMAs, one-pass softmax with a lazy maximum (tc_attn_wide.cu)
 // transposed ragged attention (keys as MMA rows) for requests with <= 64 query rows, d = 128
 bool tc_attention_narrow_supported(int d, int max_rows);
-// yh > 1: the standard form (Eq.(12)): U [N_t x yh d], keys [T2 x yh d], item.pad = head (api.cu)
+// yh > 1: the standard form (Eq.(12)): U [N_t x yh d], keys [T2 x yh d], item.pad = head (api.cu);
+// ncols = 64 or 32 query columns (every item of the launch has nq <= ncols)
 cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
                                 const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
-                                cudaStream_t st, int yh = 1);
+                                cudaStream_t st, int yh, int ncols);
 bool tc_attention_wide_supported(int d);
 // The target-side update of one layer boundary as ONE kernel (d = 128; tc_chain.cu):
 //   mode 0 (first): q(1) = LN(SwiGLUFFN(x_t)) -> U(1);  1 (mid): o(i) -> Z, ocat; c = ocat[:, :(i+1)d] W_C;

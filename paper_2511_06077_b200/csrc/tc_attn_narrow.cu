@@ -38,16 +38,18 @@ namespace tc {
 
 bool make_map_bf16(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 
+template <int NQ_>
 struct NCfg {
-  static constexpr int D = 128, BK = 128, NQ = 64;    // d, keys per tile, query columns
+  static constexpr int D = 128, BK = 128, NQ = NQ_;   // d, keys per tile, query columns (64 or 32)
+  static constexpr int CW = NQ / 4;                    // query columns per softmax warp (4 column groups)
   static constexpr int X_BYTES = BK * D * 2;           // 2 boxes of 128 keys x 64 d (16 KB each)
   // 5 stages: a tile holds its slot from the TMA issue until its PV completes (~2 slots busy with
   // S / softmax / PV), so the slots left in flight bound the HBM bytes in flight per SM; the L2
   // prefetch (STCA_NARROW_PF tiles ahead) takes the HBM latency off the ring.  SMEM: 226.3 of 227 KB.
   static constexpr int STAGES = 5;
-  static constexpr int P_BYTES = BK * NQ * 2;          // P^T: 128 keys x 64 queries, SW128 (16 KB)
+  static constexpr int P_BYTES = BK * NQ * 2;          // P^T: 128 keys x NQ queries, SW128 (NQ = 64) / SW64 (NQ = 32)
   static constexpr int U_BYTES = NQ * D * 2;           // U: 64 queries x 128 d, 2 boxes of 8 KB
-  static constexpr int RED_BYTES = 4 * 4 * 16 * 4;     // [column group][quarter][16] column partials
+  static constexpr int RED_BYTES = 4 * 4 * CW * 4;     // [column group][quarter][CW] column partials
   static constexpr int NSW = 16, THREADS = (NSW + 3) * 32;  // softmax warps; + producer, S / PV issuers
   static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + 2 * U_BYTES + RED_BYTES + 64 + 256;
   static constexpr uint32_t TS = 0, TO = 128;          // S^T buffers at 0 / 64, O^T buffers at 128 / 192
@@ -56,12 +58,13 @@ struct NCfg {
 // instruction descriptor with both operands MN-major (A = X~^T, B = P^T)
 __host__ __device__ constexpr uint32_t idesc_bf16_mn(uint32_t M, uint32_t N) { return idesc_bf16(M, N, 1) | (1u << 15); }
 
-// v[c], c < 16, across the warp's 32 lanes -> lane i returns op over all lanes of v[i & 15]
-// (recursive halving over lane bits 3..0, then one butterfly over bit 4: 16 shuffles)
-template <bool MAX>
-__device__ __forceinline__ float xreduce16(float (&v)[16], int lane) {
+// v[c], c < N (16 or 8), across the warp's 32 lanes -> lane i returns op over all lanes of v[i % N]
+// (recursive halving over lane bits log2(N)-1..0, then butterflies over the remaining lane bits:
+// 16 shuffles for N = 16, 9 for N = 8)
+template <bool MAX, int N>
+__device__ __forceinline__ float xreduce(float (&v)[N], int lane) {
 #pragma unroll
-  for (int s = 8; s >= 1; s >>= 1) {
+  for (int s = N / 2; s >= 1; s >>= 1) {
     const bool up = lane & s;
 #pragma unroll
     for (int i = 0; i < s; ++i) {
@@ -70,16 +73,32 @@ __device__ __forceinline__ float xreduce16(float (&v)[16], int lane) {
       v[i] = MAX ? fmaxf(keep, recv) : keep + recv;
     }
   }
-  const float o = __shfl_xor_sync(0xffffffffu, v[0], 16);
-  return MAX ? fmaxf(v[0], o) : v[0] + o;
+  float r = v[0];
+#pragma unroll
+  for (int s = N; s < 32; s <<= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, r, s);
+    r = MAX ? fmaxf(r, o) : r + o;
+  }
+  return r;
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_ld16(taddr, r);
+  else tmem_ld8(taddr, r);
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_st16(taddr, r);
+  else tmem_st8(taddr, r);
 }
 
 // PERSISTENT: CTA c runs items cta_items[cta_off[c] .. cta_off[c+1]) back to back (host LPT plan);
 // the X~ ring, the S / P double buffers and their barriers run across items, U (by TMA) and O^T are
 // double-buffered per item, so the next item's first tiles load and multiply while this item's
 // sums are reduced and its outputs written.
-template <bool STD>
-__global__ void __launch_bounds__(NCfg::THREADS, 1)
+template <bool STD, int NQ>
+__global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
     k_tc_attention_narrow(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapU,
                           const AttnItem *__restrict__ items, const int32_t *__restrict__ cta_off,
                           const int32_t *__restrict__ cta_items, bf16 *__restrict__ Y, float *__restrict__ part,
@@ -88,14 +107,15 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
   // yh = h: the STANDARD form (Eq.(12), stca_set_attention_form): U [N_t x h d] holds per head r the query
   // q W_Q^r (zero-padded to d columns) and the keys are K/V rows [T' x h d] holding [K^r | V^r | 0] per
   // head; item.pad = r selects the 128-column block of both, and the output row of query t is t h + r.
-  using C = NCfg;
+  using C = NCfg<NQ>;
+  constexpr int CW = C::CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sX = smem;
   uint8_t *sP = sX + C::STAGES * C::X_BYTES;
   uint8_t *sU = sP + 2 * C::P_BYTES;                                   // 2 buffers
   float *sRed = reinterpret_cast<float *>(sU + 2 * C::U_BYTES);        // [4][4][16]
-  uint32_t *sFlag = reinterpret_cast<uint32_t *>(sRed + 4 * 4 * 16);   // [tile parity][column group]: 4 byte flags
+  uint32_t *sFlag = reinterpret_cast<uint32_t *>(sRed + 4 * 4 * CW);   // [tile parity][column group]: 4 byte flags
   uint64_t *bar = reinterpret_cast<uint64_t *>(sFlag + 16);
   uint64_t *u_full = bar;                      // 2 (TMA)
   uint64_t *u_free = u_full + 2;               // 2 (S issuer commit after an item's last S)
@@ -228,9 +248,12 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
           tc_fence_after();
           const uint32_t xs = aX + s * C::X_BYTES, ps = aP + b * C::P_BYTES;
 #pragma unroll
-          for (int k = 0; k < C::BK / 16; ++k)  // 16 keys per MMA: 2 swizzle atoms of 8 key rows
-            umma_f16_ss(tmem + C::TO + ob * C::NQ, sdesc_sw128(xs + k * 2048, C::X_BYTES / 2, 1024),
-                        sdesc_sw128(ps + k * 2048, C::P_BYTES, 1024), idesc_o, (j | k) != 0);
+          for (int k = 0; k < C::BK / 16; ++k) {  // 16 keys per MMA: 2 swizzle atoms of 8 key rows
+            const uint64_t bd = NQ == 64 ? sdesc_sw128(ps + k * 2048, C::P_BYTES, 1024)  // P^T rows of 128 B
+                                         : sdesc_sw64(ps + k * 1024, C::P_BYTES, 512);   // P^T rows of 64 B
+            umma_f16_ss(tmem + C::TO + ob * C::NQ, sdesc_sw128(xs + k * 2048, C::X_BYTES / 2, 1024), bd, idesc_o,
+                        (j | k) != 0);
+          }
           umma_commit(&pv_done[b]);
           umma_commit(&x_empty[s]);
           if (++s == C::STAGES) s = 0;
@@ -245,9 +268,9 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
     for (int n = i0; n < i1; ++n) {
       const AttnItem it = items[cta_items[n]];
       const int ni = n - i0, ob = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
-      float mref[16], l[16];
+      float mref[CW], l[CW];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < CW; ++c) {
         mref[c] = -INFINITY;
         l[c] = 0.f;
       }
@@ -255,8 +278,8 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         const int b = g & 1;
         mbar_wait(&s_full[b], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t sr[16];
-        tmem_ld16(tmem + lanes + C::TS + b * C::NQ + 16 * cg, sr);
+        uint32_t sr[CW];
+        tmem_ldn<CW>(tmem + lanes + C::TS + b * C::NQ + CW * cg, sr);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -264,27 +287,27 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         const bool kv = key < it.klen - j * C::BK;
         float dm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 16; ++c) dm[c & 3] = fmaxf(dm[c & 3], __uint_as_float(sr[c]) - mref[c]);
+        for (int c = 0; c < CW; ++c) dm[c & 3] = fmaxf(dm[c & 3], __uint_as_float(sr[c]) - mref[c]);
         const bool need = kv && fmaxf(fmaxf(dm[0], dm[1]), fmaxf(dm[2], dm[3])) > STCA_NARROW_LAZY;
         const uint32_t wneed = __any_sync(0xffffffffu, need);
         uint8_t *flags = reinterpret_cast<uint8_t *>(sFlag + 4 * b + cg);
         if (lane == 0) flags[q] = (uint8_t)wneed;
         named_bar_sync(1 + cg, 128);
         if (*reinterpret_cast<volatile uint32_t *>(flags) != 0) {  // column maxima of this key tile (rare)
-          float v[16];
+          float v[CW];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) v[c] = kv ? __uint_as_float(sr[c]) : -INFINITY;
-          const float red = xreduce16<true>(v, lane);
-          if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
+          for (int c = 0; c < CW; ++c) v[c] = kv ? __uint_as_float(sr[c]) : -INFINITY;
+          const float red = xreduce<true, CW>(v, lane);
+          if (lane < CW) sRed[(cg * 4 + q) * CW + lane] = red;
           named_bar_sync(1 + cg, 128);
-          float f[16];
+          float f[CW];
           bool any = false;
 #pragma unroll
-          for (int c = 0; c < 16; c += 4) {
-            float4 t = *reinterpret_cast<const float4 *>(sRed + (cg * 4) * 16 + c);
+          for (int c = 0; c < CW; c += 4) {
+            float4 t = *reinterpret_cast<const float4 *>(sRed + (cg * 4) * CW + c);
 #pragma unroll
             for (int qq = 1; qq < 4; ++qq) {
-              const float4 u = *reinterpret_cast<const float4 *>(sRed + (cg * 4 + qq) * 16 + c);
+              const float4 u = *reinterpret_cast<const float4 *>(sRed + (cg * 4 + qq) * CW + c);
               t = make_float4(fmaxf(t.x, u.x), fmaxf(t.y, u.y), fmaxf(t.z, u.z), fmaxf(t.w, u.w));
             }
             const float tm[4] = {t.x, t.y, t.z, t.w};
@@ -297,22 +320,22 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
             }
           }
 #pragma unroll
-          for (int c = 0; c < 16; ++c) l[c] *= f[c];
+          for (int c = 0; c < CW; ++c) l[c] *= f[c];
           if (__any_sync(0xffffffffu, any)) {  // rescale O^T columns once the PVs issued so far are done
             mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
-            uint32_t o[16];
-            tmem_ld16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);
+            uint32_t o[CW];
+            tmem_ldn<CW>(tmem + lanes + C::TO + ob * C::NQ + CW * cg, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f[c]);
-            tmem_st16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);
+            for (int c = 0; c < CW; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f[c]);
+            tmem_stn<CW>(tmem + lanes + C::TO + ob * C::NQ + CW * cg, o);
             tmem_st_wait();
           }
         }
-        uint32_t w[8];
+        uint32_t w[CW / 2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < CW / 2; ++i) {
           const float p0 = kv ? ex2(__uint_as_float(sr[2 * i]) - mref[2 * i]) : 0.f;
           const float p1 = kv ? ex2(__uint_as_float(sr[2 * i + 1]) - mref[2 * i + 1]) : 0.f;
           l[2 * i] += p0;
@@ -321,8 +344,10 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
         }
         if (g >= 2) mbar_wait(&pv_done[b], ((g - 2) >> 1) & 1);  // PV of tile g-2 has read P^T buffer b
         uint8_t *prow = sP + b * C::P_BYTES;
-        *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg)) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4 *>(prow + sw128_off(key, 2 * cg + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k)
+          *reinterpret_cast<uint4 *>(prow + (NQ == 64 ? sw128_off(key, 2 * cg + k) : sw64_off(key, cg))) =
+              make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
         fence_proxy_async();
         tc_fence_before();
         __syncwarp();
@@ -331,26 +356,26 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
       // ---- sums over the keys: per warp by recursive halving, then the 4 lane quarters through SMEM ----
       named_bar_sync(1 + cg, 128);  // the last tile's sRed reads are done
       {
-        const float red = xreduce16<false>(l, lane);
-        if (lane < 16) sRed[(cg * 4 + q) * 16 + lane] = red;
+        const float red = xreduce<false, CW>(l, lane);
+        if (lane < CW) sRed[(cg * 4 + q) * CW + lane] = red;
       }
       if (nt >= 1) mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);  // the item's last PV
       tc_fence_before();
       named_bar_sync(1 + cg, 128);
       tc_fence_after();
-      uint32_t o[16];
-      tmem_ld16(tmem + lanes + C::TO + ob * C::NQ + 16 * cg, o);  // thread = output column d, 16 queries
+      uint32_t o[CW];
+      tmem_ldn<CW>(tmem + lanes + C::TO + ob * C::NQ + CW * cg, o);  // thread = output column d, CW queries
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[ob]);  // the PV issuer may start item ni + 2 in this buffer
       const int d = key;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int qn = 16 * cg + e;
+      for (int e = 0; e < CW; ++e) {
+        const int qn = CW * cg + e;
         if (qn < it.nq) {
-          const float ln = sRed[(cg * 4) * 16 + e] + sRed[(cg * 4 + 1) * 16 + e] + sRed[(cg * 4 + 2) * 16 + e] +
-                           sRed[(cg * 4 + 3) * 16 + e];
+          const float ln = sRed[(cg * 4) * CW + e] + sRed[(cg * 4 + 1) * CW + e] + sRed[(cg * 4 + 2) * CW + e] +
+                           sRed[(cg * 4 + 3) * CW + e];
           const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
           if (it.part_row < 0) {
             if constexpr (STD) Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
@@ -371,29 +396,40 @@ __global__ void __launch_bounds__(NCfg::THREADS, 1)
 
 }  // namespace tc
 
-bool tc_attention_narrow_supported(int d, int max_rows) { return d == 128 && max_rows <= tc::NCfg::NQ; }
+bool tc_attention_narrow_supported(int d, int max_rows) { return d == 128 && max_rows <= 64; }
 
-cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
-                                const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
-                                cudaStream_t st, int yh) {
-  using C = tc::NCfg;
-  if (n_ctas <= 0) return cudaSuccess;
+// ncols = 64 or 32: the query columns of the instantiation (a request with m_b h <= 32 takes the
+// 32-column kernel: half the MMA N, the exponentials and the softmax registers of the 64-column one)
+template <int NQ>
+static cudaError_t narrow_launch(const void *U, int64_t NQrows, const void *Xt, int64_t T2, const AttnItem *items,
+                                 const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
+                                 cudaStream_t st, int yh) {
+  using C = tc::NCfg<NQ>;
   CUtensorMap mx, mu;
   // standard form (yh = h): U is [N_t x h d], the keys [T' x h d]; an item reads one d-column block of each
   const int64_t cols = (int64_t)C::D * yh;
-  if (!tc::make_map_bf16(&mx, Xt, T2, cols, cols, C::BK) || !tc::make_map_bf16(&mu, U, NQ / yh, cols, cols, C::NQ))
+  if (!tc::make_map_bf16(&mx, Xt, T2, cols, cols, C::BK) || !tc::make_map_bf16(&mu, U, NQrows / yh, cols, cols, C::NQ))
     return cudaErrorInvalidValue;
-  // two instantiations: the standard form's per-item head offsets cost the reordered form registers
+  // separate instantiations: the standard form's per-item head offsets cost the reordered form registers
   // (spill loads 60 -> 316 bytes, +12-18 % at multi / train) when compiled into one kernel
-  const void *kfn = yh > 1 ? (const void *)tc::k_tc_attention_narrow<true> : (const void *)tc::k_tc_attention_narrow<false>;
+  const void *kfn = yh > 1 ? (const void *)tc::k_tc_attention_narrow<true, NQ> : (const void *)tc::k_tc_attention_narrow<false, NQ>;
   cudaError_t e0 = smem_optin(kfn, C::SMEM);
   if (e0 != cudaSuccess) return e0;
   note_launch();
   if (yh > 1)
-    return launch_pdl(tc::k_tc_attention_narrow<true>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx,
-                      mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
-  return launch_pdl(tc::k_tc_attention_narrow<false>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st, mx,
-                    mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
+    return launch_pdl(tc::k_tc_attention_narrow<true, NQ>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM,
+                      st, mx, mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
+  return launch_pdl(tc::k_tc_attention_narrow<false, NQ>, dim3((unsigned)n_ctas), dim3(C::THREADS), (size_t)C::SMEM, st,
+                    mx, mu, items, cta_off, cta_items, (bf16 *)Y, part, yh);
+}
+
+cudaError_t tc_attention_narrow(const void *U, int64_t NQ, const void *Xt, int64_t T2, const AttnItem *items,
+                                const int32_t *cta_off, const int32_t *cta_items, int n_ctas, void *Y, float *part,
+                                cudaStream_t st, int yh, int ncols) {
+  if (n_ctas <= 0) return cudaSuccess;
+  if (ncols == 32) return narrow_launch<32>(U, NQ, Xt, T2, items, cta_off, cta_items, n_ctas, Y, part, st, yh);
+  if (ncols == 64) return narrow_launch<64>(U, NQ, Xt, T2, items, cta_off, cta_items, n_ctas, Y, part, st, yh);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace stca

@@ -148,13 +148,15 @@ KC_BOUND = 3 * 2.0 ** -9 + 4e-4
 
 
 @pytest.mark.parametrize("d,h,m,wq", [(128, 4, 16, 1.0), (128, 4, 64, 1.0), (128, 4, 8, 8.0), (128, 4, 64, 8.0),
+                                      (128, 4, 8, 1.0), (128, 4, 5, 1.0), (128, 4, 12, 1.0),
                                       (256, 8, 32, 1.0), (512, 8, 32, 1.0)])
 def test_attention_stage_isolated(d, h, m, wq):
     """the attention output Y of one layer against an f64 softmax over the GPU's own
     bf16 U and X~ (read back from the device), elementwise within the arithmetic's rounding bound
     KC_BOUND * A_e (the SURVEY's proposed 4e-3 row-relative bound is below the two bf16 output roundings
     the kernels do: measured 4.4-6.4e-3 row-relative; row-relative <= 1e-2 is kept as a second check).  m h <= 64 takes the
-    transposed kernel, 256 the 128-row kernel, d = 256 / 512 the wide kernel; the 9000-key history
+    transposed kernel (its 32-column instantiation for m h <= 32: m = 8 and 5, the latter with partial
+    column groups; m = 12 is 48 rows on the 64-column one), 256 the 128-row kernel, d = 256 / 512 the wide kernel; the 9000-key history
     is split into chunks and folded (split-K LSE merge); wq = 8 is the sharp-softmax regime."""
     import torch
     import paper_2511_06077_b200 as stca
