@@ -127,6 +127,10 @@ struct ProfRegion {
 
 }  // namespace
 
+// rows per block of the history backward (hist_bwd.cu): 2^18 rows keep its weight-gradient GEMMs
+// (K = rows) out of the small split-K shapes; scratch ~1.2 GB at d = 128, r = 4
+#define STCA_BWD_ROWS (1 << 18)
+
 struct LayerW {
   void *W1h = nullptr, *Woh = nullptr;  // history FFN: [d x 2rd] interleaved (u_j, v_j), [rd x d]
   float *gh = nullptr, *bh = nullptr;
@@ -1731,11 +1735,11 @@ extern "C" stca_status stca_history_backward(stca_handle *h, int32_t layer, cons
   CU(cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
   const int d = h->cfg.d, rd = h->cfg.r * d;
-  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), STCA_BWD_ROWS);
   CU(h->bwd_scratch.ensure(stca::hist_bwd_scratch_bytes(d, rd, R), st));
   LayerW &Ly = h->L[layer - 1];
   CU(stca::hist_bwd(&h->blas, (const bf16 *)X, rows, d, rd, (const bf16 *)Ly.W1cat,
-                    (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, dX, dWu, dWv, dWo, dgamma, dbeta,
+                    (const bf16 *)Ly.Woh, Ly.tc.W1h, Ly.tc.Woh, Ly.gh, h->cfg.ln_eps, dXt, dX, dWu, dWv, dWo, dgamma, dbeta,
                     h->bwd_scratch.p, R, st));
   return STCA_OK;
 }
@@ -1767,10 +1771,10 @@ static cudaError_t bwd_attn_hist(void *ctx, int layer, const float *dY, float *d
   const void *Xt = (const uint8_t *)h->xt_cache.p + (size_t)L * h->T2 * d * h->es;
   if (c.nit > 0 && (e = stca::tc_attention_bwd(U, c.NQ, Xt, h->T2, c.items, c.nit, dY, dXt, dU, c.st)) != cudaSuccess)
     return e;
-  const int64_t R = std::min<int64_t>(std::max<int64_t>(c.rows, 1), 1 << 16);
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(c.rows, 1), STCA_BWD_ROWS);
   LayerW &Ly = h->L[L];
   return stca::hist_bwd(&h->blas, (const bf16 *)c.X, c.rows, d, rd, (const bf16 *)Ly.W1cat,
-                        (const bf16 *)Ly.Woh, Ly.gh, h->cfg.ln_eps, dXt, c.dX, c.gWu[L], c.gWv[L], c.gWo[L], c.gg[L],
+                        (const bf16 *)Ly.Woh, Ly.tc.W1h, Ly.tc.Woh, Ly.gh, h->cfg.ln_eps, dXt, c.dX, c.gWu[L], c.gWv[L], c.gWo[L], c.gg[L],
                         c.gb[L], h->bwd_scratch.p, R, c.st);
 }
 
@@ -1856,7 +1860,7 @@ extern "C" stca_status stca_backward(stca_handle *h, const void *xt, int64_t Nt,
     if (s != STCA_OK) return s;
   }
   CU(h->dxt_buf.ensure((size_t)std::max<int64_t>(h->T2, 1) * d * 4, st));
-  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), 1 << 16);
+  const int64_t R = std::min<int64_t>(std::max<int64_t>(rows, 1), STCA_BWD_ROWS);
   CU(h->bwd_scratch.ensure(stca::hist_bwd_scratch_bytes(d, rd, R), st));
   CU(h->sbwd_scratch.ensure(stca::stack_bwd_scratch_bytes(d, hh, rd, M, Nt), st));
   // dX: the history backward accumulates into it; without a caller buffer it goes to scratch

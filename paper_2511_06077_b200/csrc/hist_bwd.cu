@@ -1,16 +1,16 @@
-// hist_bwd.cu -- backward of one layer's history path (partial), Eq.(1)-(2),
-// P:L103-111:  X~ = LN(SwiGLUFFN(X)) = LN((X Wu * silu(X Wv)) Wo) over the kept history rows.
+// hist_bwd.cu -- backward of one layer's history path, Eq.(1)-(2), P:L103-111:
+//   X~ = LN(SwiGLUFFN(X)) = LN((X Wu * silu(X Wv)) Wo) over the kept history rows.
 //
-// The plain GEMMs (recompute a = X Wu, g = X Wv, y = H Wo; then dH = dy Wo^T, dX = da Wu^T + dg Wv^T and
-// the weight gradients dWo = H^T dy, dWu = X^T da, dWv = X^T dg, summed over all rows) are library GEMMs
-// (cuBLAS, bf16 operands, fp32 accumulation); the two elementwise steps are kernels here:
-//   k_swiglu_fwd   h = a * silu(g) -> bf16 (the forward's rounding point of H)
-//   k_ln_bwd       per row: mu, s from y; x^ = (y - mu) / s; dx^ = dX~ * gamma;
-//                  dy = (dx^ - mean(dx^) - x^ mean(dx^ x^)) / s -> bf16; dgamma += dX~ x^, dbeta += dX~
-//   k_swiglu_bwd   da = dH silu(g), dg = dH a sig(g) (1 + g (1 - sig(g))) -> bf16
-// The intermediates are bf16 (a and g come out of ONE GEMM with [Wu | Wv], rounded like the forward's
-// operands), y stays fp32 for the LayerNorm statistics.  Rows are processed in blocks of 2^16 (working
-// set ~0.5 GB at d = 128, r = 4).  Every history row
+// Per block of rows:
+//   tc_ffn (tcgen05)        h = u silu(v) with [u | v] = X W1 (bf16, the SwiGLU epilogue: [u | v] stays on
+//                           chip), y = h Wo (fp32) -- the forward recomputed, the LayerNorm's input
+//   k_ln_bwd                per row: mu, s from y; x^ = (y - mu) / s; dx^ = dX~ * gamma;
+//                           dy = (dx^ - mean(dx^) - x^ mean(dx^ x^)) / s -> bf16; dgamma += dX~ x^, dbeta += dX~
+//   cuBLAS                  dWo += h^T dy;  dH = dy Wo^T (bf16)
+//   tc_swiglu_bwd (tcgen05) [u | v] = X W1 recomputed in TMEM, the epilogue reads dH and writes
+//                           da = dH silu(v), dv = dH u sig(v) (1 + v (1 - sig(v))) (bf16)
+//   cuBLAS                  dWu += X^T da, dWv += X^T dv;  dX += [da | dv] [Wu | Wv]^T (one GEMM, K = 2 rd)
+// (bf16 operands, fp32 accumulation.)  Rows are processed in blocks of 2^16.  Every history row
 // appears once per request however many targets share it, so the gradients are aggregated at the
 // request level by construction.
 #include <cublas_v2.h>
@@ -19,57 +19,101 @@
 #include <algorithm>
 
 #include "launch.h"
+#include "tc.h"
 
 namespace stca {
 
 namespace {
 
-__device__ __forceinline__ float silu_(float g) { return g / (1.f + __expf(-g)); }
-
-// ag = [a | g] bf16 [n x 2rd] (a = X Wu, g = X Wv from one GEMM) -> h = a silu(g) bf16 [n x rd];
-// 8 bf16 (16 bytes) per thread and access, rd % 8 == 0
-__global__ void __launch_bounds__(256) k_swiglu_fwd(const bf16 *__restrict__ ag, bf16 *__restrict__ h, int rd, int64_t n) {
-  const int per_row = rd / 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per_row; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / per_row;
-    const int j = (int)(i - r * per_row);
-    const uint4 av = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + 8 * j);
-    const uint4 gv = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + rd + 8 * j);
-    const __nv_bfloat162 *a2 = reinterpret_cast<const __nv_bfloat162 *>(&av), *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv);
-    uint4 out;
-    __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(&out);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 a = __bfloat1622float2(a2[k]), g = __bfloat1622float2(g2[k]);
-      o2[k] = __floats2bfloat162_rn(a.x * silu_(g.x), a.y * silu_(g.y));
-    }
-    *reinterpret_cast<uint4 *>(h + r * rd + 8 * j) = out;
-  }
+__device__ __forceinline__ uint32_t pack_bf16r(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&v);
 }
 
-// dag = [da | dg] bf16 [n x 2rd]: da = dH silu(g), dg = dH a sig(g) (1 + g (1 - sig(g)))
-__global__ void __launch_bounds__(256) k_swiglu_bwd(const bf16 *__restrict__ ag, const bf16 *__restrict__ dh,
-                                                    bf16 *__restrict__ dag, int rd, int64_t n) {
-  const int per_row = rd / 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per_row; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / per_row;
-    const int j = (int)(i - r * per_row);
-    const uint4 av = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + 8 * j);
-    const uint4 gv = *reinterpret_cast<const uint4 *>(ag + r * 2 * rd + rd + 8 * j);
-    const uint4 dv = *reinterpret_cast<const uint4 *>(dh + r * rd + 8 * j);
-    const __nv_bfloat162 *a2 = reinterpret_cast<const __nv_bfloat162 *>(&av), *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv),
-                         *d2 = reinterpret_cast<const __nv_bfloat162 *>(&dv);
-    uint4 oa, og;
-    __nv_bfloat162 *oa2 = reinterpret_cast<__nv_bfloat162 *>(&oa), *og2 = reinterpret_cast<__nv_bfloat162 *>(&og);
+// d = 128: a lane owns 4 consecutive columns (16-byte loads of y, dX~ and gamma, 8-byte stores of dy),
+// a warp takes TWO rows per step with their shuffle reductions interleaved (the one-row, scalar-load
+// form below ran at ~2.5 TB/s: latency-bound on its dependent warp sums)
+__device__ __forceinline__ void warp_sum2(float &a, float &b) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+}
+__global__ void __launch_bounds__(256) k_ln_bwd128(const float *__restrict__ y, const float *__restrict__ dXt,
+                                                   const float *__restrict__ gamma, int64_t rows, float eps,
+                                                   bf16 *__restrict__ dy, float *__restrict__ dgam,
+                                                   float *__restrict__ dbet) {
+  constexpr int D = 128;
+  extern __shared__ float acc[];  // [8 warps][2][D]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4 gm = reinterpret_cast<const float4 *>(gamma)[lane];
+  float ga[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * 2; r0 < rows; r0 += (int64_t)gridDim.x * 16) {
+    float yv[2][4], dv[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool in = r0 + t < rows;
+      const float4 a = in ? __ldg(reinterpret_cast<const float4 *>(y + (r0 + t) * D) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 b = in ? __ldg(reinterpret_cast<const float4 *>(dXt + (r0 + t) * D) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+      yv[t][0] = a.x; yv[t][1] = a.y; yv[t][2] = a.z; yv[t][3] = a.w;
+      dv[t][0] = b.x; dv[t][1] = b.y; dv[t][2] = b.z; dv[t][3] = b.w;
+    }
+    float s0 = (yv[0][0] + yv[0][1]) + (yv[0][2] + yv[0][3]), s1 = (yv[1][0] + yv[1][1]) + (yv[1][2] + yv[1][3]);
+    warp_sum2(s0, s1);
+    const float mu[2] = {s0 / D, s1 / D};
+    float q0 = 0.f, q1 = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float2 a = __bfloat1622float2(a2[k]), g = __bfloat1622float2(g2[k]), d = __bfloat1622float2(d2[k]);
-      const float sx = 1.f / (1.f + __expf(-g.x)), sy = 1.f / (1.f + __expf(-g.y));
-      oa2[k] = __floats2bfloat162_rn(d.x * g.x * sx, d.y * g.y * sy);
-      og2[k] = __floats2bfloat162_rn(d.x * a.x * sx * (1.f + g.x * (1.f - sx)), d.y * a.y * sy * (1.f + g.y * (1.f - sy)));
+      q0 += (yv[0][k] - mu[0]) * (yv[0][k] - mu[0]);
+      q1 += (yv[1][k] - mu[1]) * (yv[1][k] - mu[1]);
     }
-    *reinterpret_cast<uint4 *>(dag + r * 2 * rd + 8 * j) = oa;
-    *reinterpret_cast<uint4 *>(dag + r * 2 * rd + rd + 8 * j) = og;
+    warp_sum2(q0, q1);
+    const float inv[2] = {rsqrtf(q0 / D + eps), rsqrtf(q1 / D + eps)};
+    const float g4[4] = {gm.x, gm.y, gm.z, gm.w};
+    float m1[2] = {0.f, 0.f}, m2[2] = {0.f, 0.f}, gv[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool in = r0 + t < rows;  // a missing second row has dv = 0: no gradient contribution
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (yv[t][k] - mu[t]) * inv[t], g = dv[t][k];
+        if (in) {
+          ga[k] += g * xh;
+          ba[k] += g;
+        }
+        gv[t][k] = g * g4[k];
+        yv[t][k] = xh;
+        m1[t] += gv[t][k];
+        m2[t] += gv[t][k] * xh;
+      }
+    }
+    warp_sum2(m1[0], m1[1]);
+    warp_sum2(m2[0], m2[1]);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (r0 + t >= rows) break;
+      const float a = m1[t] / D, b = m2[t] / D;
+      uint2 o;
+      o.x = pack_bf16r((gv[t][0] - a - yv[t][0] * b) * inv[t], (gv[t][1] - a - yv[t][1] * b) * inv[t]);
+      o.y = pack_bf16r((gv[t][2] - a - yv[t][2] * b) * inv[t], (gv[t][3] - a - yv[t][3] * b) * inv[t]);
+      reinterpret_cast<uint2 *>(dy + (r0 + t) * D)[lane] = o;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    acc[(w * 2) * D + 4 * lane + k] = ga[k];
+    acc[(w * 2 + 1) * D + 4 * lane + k] = ba[k];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+    float sg = 0.f, sb = 0.f;
+    for (int q = 0; q < 8; ++q) {
+      sg += acc[(q * 2) * D + e];
+      sb += acc[(q * 2 + 1) * D + e];
+    }
+    atomicAdd(dgam + e, sg);
+    atomicAdd(dbet + e, sb);
   }
 }
 
@@ -152,13 +196,13 @@ cublasStatus_t gemm_rm(cublasHandle_t hb, bool ta, bool tb, int m, int n, int k,
 
 }  // namespace
 
-// Scratch is the caller's: ag, dag bf16 [R x 2rd]; h, dh bf16 [R x rd]; y fp32 [R x d]; dy bf16 [R x d]
+// Scratch is the caller's: dag bf16 [R x 2rd]; h, dh bf16 [R x rd]; y fp32 [R x d]; dy bf16 [R x d]
 size_t hist_bwd_scratch_bytes(int d, int rd, int64_t R) {
-  return (size_t)R * rd * (4 * 2 + 2 * 2) + (size_t)R * d * (4 + 2) + 4096;
+  return (size_t)R * rd * (2 * 2 + 2 * 2) + (size_t)R * d * (4 + 2) + 4096;
 }
 
 cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, const bf16 *W1, const bf16 *Wo,
-                     const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
+                     const void *W1t, const void *Wot, const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
                      float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st) {
   if (!*blas) {
     cublasHandle_t hb;
@@ -173,7 +217,7 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
     p += (bytes + 255) / 256 * 256;
     return q;
   };
-  bf16 *ag = (bf16 *)take((size_t)R * 2 * rd * 2), *dag = (bf16 *)take((size_t)R * 2 * rd * 2);
+  bf16 *dag = (bf16 *)take((size_t)R * 2 * rd * 2);
   bf16 *h = (bf16 *)take((size_t)R * rd * 2), *dh = (bf16 *)take((size_t)R * rd * 2);
   float *y = (float *)take((size_t)R * d * 4);
   bf16 *dy = (bf16 *)take((size_t)R * d * 2);
@@ -187,17 +231,17 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
   for (int64_t r0 = 0; r0 < rows; r0 += R) {
     const int n = (int)std::min<int64_t>(R, rows - r0);
     const bf16 *Xb = X + r0 * d;
-    // recompute the forward: [a | g] = X [Wu | Wv] (one GEMM, bf16), h = a silu(g) (bf16), y = h Wo (fp32)
-    if (gemm_rm(hb, false, false, n, 2 * rd, d, Xb, d, W1, 2 * rd, ag, 2 * rd, 0.f, true) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
-    note_launch(3);
-    k_swiglu_fwd<<<4 * ew, 256, 0, st>>>(ag, h, rd, (int64_t)n);
-    if (gemm_rm(hb, false, false, n, d, rd, h, rd, Wo, d, y, d, 0.f) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    // recompute the forward on tcgen05 (tc_ffn: the SwiGLU epilogue writes h = u silu(v) in bf16 and
+    // [u | v] never reaches HBM; y = h Wo in fp32, the LayerNorm's input)
+    if ((e = tc_ffn(Xb, d, n, W1t, Wot, d, rd, nullptr, nullptr, 0.f, nullptr, 0, y, d, h, st)) != cudaSuccess) return e;
+    note_launch(1);
     // LayerNorm backward -> dy (bf16), dgamma, dbeta
     {
       const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * ew);
       const size_t sm = 16 * d * sizeof(float);
-      if (d <= 128) k_ln_bwd<4><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
+      if (d == 128) k_ln_bwd128<<<(unsigned)std::min<int64_t>((n + 15) / 16, 4 * ew), 256, sm, st>>>(
+          y, dXt + r0 * d, gamma, n, eps, dy, dgam, dbet);
+      else if (d <= 128) k_ln_bwd<4><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
       else if (d <= 256) k_ln_bwd<8><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
       else k_ln_bwd<16><<<g, 256, sm, st>>>(y, dXt + r0 * d, gamma, d, n, eps, dy, dgam, dbet);
     }
@@ -205,7 +249,8 @@ cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, co
     if (gemm_rm(hb, true, false, rd, d, n, h, rd, dy, d, dWo, d, 1.f) != CUBLAS_STATUS_SUCCESS ||
         gemm_rm(hb, false, true, n, rd, d, dy, d, Wo, d, dh, rd, 0.f, true) != CUBLAS_STATUS_SUCCESS)
       return cudaErrorUnknown;
-    k_swiglu_bwd<<<4 * ew, 256, 0, st>>>(ag, dh, dag, rd, (int64_t)n);
+    // [da | dg] from the recomputed [u | v] = X W1 (tcgen05, in the GEMM's epilogue) and dH
+    if ((e = tc_swiglu_bwd(Xb, d, n, W1t, d, rd, dh, rd, dag, 2 * rd, st)) != cudaSuccess) return e;
     // dWu += X^T da, dWv += X^T dg;  dX += [da | dg] [Wu | Wv]^T (one GEMM, K = 2 rd)
     float *dXb = dX + r0 * d;
     if (gemm_rm(hb, true, false, d, rd, n, Xb, d, dag, 2 * rd, dWu, rd, 1.f) != CUBLAS_STATUS_SUCCESS ||

@@ -75,7 +75,7 @@ cudaError_t peer_exchange(const PeerMerge &pm, int G, cudaStream_t st);
 size_t hist_bwd_scratch_bytes(int d, int rd, int64_t R);
 // W1 = [Wu | Wv] bf16 [d x 2rd] (column blocks), Wo bf16 [rd x d]
 cudaError_t hist_bwd(void **blas, const bf16 *X, int64_t rows, int d, int rd, const bf16 *W1, const bf16 *Wo,
-                     const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
+                     const void *W1t, const void *Wot, const float *gamma, float eps, const float *dXt, float *dX, float *dWu, float *dWv, float *dWo,
                      float *dgam, float *dbet, void *scratch, int64_t R, cudaStream_t st);
 void hist_bwd_release(void *blas);
 

@@ -60,6 +60,9 @@ cudaError_t tc_project(const TcProj &p, cudaStream_t st);
 cudaError_t tc_ffn(const void *in, int64_t ldi, int64_t rows, const void *W1, const void *Wo, int d, int rd,
                    const float *g, const float *b, float eps, void *out_s, int64_t ldo, float *out_f, int64_t ldof,
                    void *H, cudaStream_t st);
+// SwiGLU gate backward on the recomputed [u | v] = X W1 (hist_bwd.cu): da -> dag[:, :rd], dv -> dag[:, rd:]
+cudaError_t tc_swiglu_bwd(const void *X, int64_t ldx, int64_t rows, const void *W1, int d, int rd, const void *dH,
+                          int64_t ldh, void *dag, int64_t lddag, cudaStream_t st);
 // C[M x N] = A[M x K] (bf16, lda) . B where Bt = B^T [N x K] bf16 K-major
 cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N, int K, void *Cs, int64_t ldcs,
                     float *Cf, int64_t ldcf, cudaStream_t st);

@@ -12,6 +12,9 @@
 //                H[:, 32c+j] = u * silu(v) -> bf16   (Eq.(1))
 //   TEPI_LN     : BN == N == d: LayerNorm over the row (biased variance, eps inside sqrt)
 //                -> bf16 / fp32                       (Eq.(2)-(3))
+//   TEPI_SWIGLU_BWD : the backward of the SwiGLU gate (NEXT-1, hist_bwd.cu) on the recomputed
+//                [u | v] chunks of TEPI_SWIGLU's layout: with dH read from global (aux, row-major),
+//                da = dH silu(v) -> Cs[:, j], dv = dH u sig(v) (1 + v (1 - sig(v))) -> Cs[:, off2 + j]
 // Used for the target-side contractions (U = q W_QK, o = Y W_VO, [o|x_t] W_C, W_Z) and
 // the query-side SwiGLUFFN instances.
 #include <cudaTypedefs.h>
@@ -28,7 +31,7 @@
 namespace stca {
 namespace tc {
 
-enum { TEPI_STORE = 0, TEPI_SWIGLU = 1, TEPI_LN = 2 };
+enum { TEPI_STORE = 0, TEPI_SWIGLU = 1, TEPI_LN = 2, TEPI_SWIGLU_BWD = 3 };
 
 struct EpiArgs {
   bf16 *Cs;
@@ -37,6 +40,8 @@ struct EpiArgs {
   int64_t ldcf;
   const float *g, *b;
   float eps;
+  const bf16 *aux;  // TEPI_SWIGLU_BWD: dH [M x N/2] bf16, row stride ldaux; dv at column off2 of Cs
+  int64_t ldaux, off2;
 };
 
 // u * silu(v) = u v sigmoid(v) = a + a tanh(v / 2) with a = u v / 2: one MUFU op per output
@@ -179,12 +184,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = q * 32 + lane;
     uint8_t *hstg = stg + hg * C::STG_BYTES;
     // columns of the accumulator this half group owns (a half group may own none for tiny BN)
-    constexpr int GRAN = EPI == TEPI_SWIGLU ? 64 : 32;
+    constexpr bool GATE = EPI == TEPI_SWIGLU || EPI == TEPI_SWIGLU_BWD;  // [u 32 | v 32] column blocks
+    constexpr int GRAN = GATE ? 64 : 32;
     constexpr bool SPLIT = BN >= 2 * GRAN;
     constexpr int HCOLS = SPLIT ? BN / 2 : BN;
     const int c_lo = SPLIT ? hg * HCOLS : 0;
     const bool active = SPLIT || hg == 0;
-    constexpr int OUT_COLS = EPI == TEPI_SWIGLU ? BN / 2 : BN;  // output columns of a tile
+    constexpr int OUT_COLS = GATE ? BN / 2 : BN;  // output columns of a tile
     if (EPI == TEPI_LN) {  // gamma/beta from SMEM: global loads in flight stall this warp's tcgen05.ld
       for (int c = threadIdx.x; c < BN; c += 256) {
         lnp[c] = ea.g[c];
@@ -192,16 +198,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       named_bar_sync(3, 256);
     }
+    // TEPI_SWIGLU_BWD: this thread's row of dH for its half group's hidden columns (HCOLS / 2 bf16,
+    // contiguous) is loaded one tile AHEAD into registers: eight epilogue warps with one 64-byte load
+    // each in flight left the kernel at ~2.5 TB/s (latency-bound), ncu l4_hist_bwd
+    constexpr int NBW = EPI == TEPI_SWIGLU_BWD ? HCOLS / 16 : 1;
+    uint4 dh_nxt[NBW];
+    auto fetch_dh = [&](int pp) {
+      if constexpr (EPI == TEPI_SWIGLU_BWD) {
+        const int mm = (2 * (pp / tn) + (int)crank) * C::BM, nn = (pp % tn) * BN;
+        const int64_t gr = (int64_t)mm + row;
+        const bool ok = pp < npairs && gr < M;
+        const uint4 *src = reinterpret_cast<const uint4 *>(ea.aux + (ok ? gr : 0) * ea.ldaux + nn / 2 + c_lo / 2);
+#pragma unroll
+        for (int k = 0; k < NBW; ++k) dh_nxt[k] = ok ? __ldg(src + k) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    fetch_dh(cid);
     int i = 0;
     for (int p = cid; p < npairs; p += ncl, ++i) {
       const int m0 = (2 * (p / tn) + (int)crank) * C::BM, n0 = (p % tn) * BN;
-      const int64_t out_n0 = EPI == TEPI_SWIGLU ? n0 / 2 : n0;
+      const int64_t out_n0 = GATE ? n0 / 2 : n0;
       const int a = i % C::NACC;
       mbar_wait(&acc_full[a], (i / C::NACC) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + a * C::TMEM_COLS + ((uint32_t)(q * 32) << 16) + c_lo;
       // stage output block `blk` (32 output columns of the tile, fp32 or bf16 rows), then store it
-      auto emit = [&](int blk, const float (&y)[32], bool f32) {
+      auto emit = [&](int blk, const float (&y)[32], bool f32, int64_t coff = 0) {
         const int RS = f32 ? C::F_STRIDE : C::H_STRIDE, ES = f32 ? 4 : 2;
         uint8_t *srow = hstg + row * RS;
         if (f32) {
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int c = ltid; c < (128 << sh); c += 128) {
           const int rr = c >> sh, ch = c & ((1 << sh) - 1);
           if ((int64_t)m0 + rr < M)
-            *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + out_n0 + blk * 32) * ES + ch * 16) =
+            *reinterpret_cast<uint4 *>(dst + (((int64_t)m0 + rr) * ld + coff + out_n0 + blk * 32) * ES + ch * 16) =
                 *reinterpret_cast<const uint4 *>(hstg + rr * RS + ch * 16);
         }
         named_bar_sync(1 + hg, 128);  // the staging block may be rewritten
@@ -266,6 +288,45 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             emit((c_lo + c) / 64, y, false);
             tmem_ld_wait();
           }
+        }
+      } else if (EPI == TEPI_SWIGLU_BWD) {
+        uint4 dcur[NBW];
+#pragma unroll
+        for (int k = 0; k < NBW; ++k) dcur[k] = dh_nxt[k];
+        fetch_dh(p + ncl);  // the next tile's dH, in flight during this tile
+#pragma unroll
+        for (int c = 0; c < HCOLS; c += 64) {
+          const int blk = (c_lo + c) / 64;
+          uint32_t u[32], v[32];
+          tmem_ld32(taddr + c, u);
+          tmem_ld32(taddr + c + 32, v);
+          float dh[32];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint4 w = dcur[(c / 64) * 4 + k];
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&ww[t]));
+              dh[8 * k + 2 * t] = f.x;
+              dh[8 * k + 2 * t + 1] = f.y;
+            }
+          }
+          tmem_ld_wait();
+          float y[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {  // sig(v) = 1/2 + tanh(v/2)/2 (one MUFU op, as the forward)
+            const float vv = __uint_as_float(v[e]);
+            float t;
+            asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * vv));
+            const float sg = fmaf(0.5f, t, 0.5f);
+            y[e] = dh[e] * vv * sg;                                                                 // da
+            v[e] = __float_as_uint(dh[e] * __uint_as_float(u[e]) * sg * fmaf(vv, 1.f - sg, 1.f));  // dv
+          }
+          emit(blk, y, false);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(v[e]);
+          emit(blk, y, false, ea.off2);
         }
       } else if (active) {  // TEPI_LN over BN == d columns
         // one statistics pass over the half row, sums shifted by its first value (no cancellation
@@ -435,6 +496,11 @@ static cudaError_t gemm_dispatch(int epi, const void *A, int64_t lda, const void
     if (N % 64 == 0) G(64, TEPI_SWIGLU);
     return cudaErrorInvalidValue;
   }
+  if (epi == TEPI_SWIGLU_BWD) {
+    if (N % 256 == 0) G(256, TEPI_SWIGLU_BWD);
+    if (N % 128 == 0) G(128, TEPI_SWIGLU_BWD);
+    return cudaErrorInvalidValue;
+  }
   if (N % 256 == 0) G(256, TEPI_STORE);
   if (N % 128 == 0) G(128, TEPI_STORE);
   if (N % 64 == 0) G(64, TEPI_STORE);
@@ -446,6 +512,15 @@ cudaError_t tc_gemm(const void *A, int64_t lda, const void *Bt, int64_t M, int N
                     float *Cf, int64_t ldcf, cudaStream_t st) {
   tc::EpiArgs ea{(bf16 *)Cs, ldcs, Cf, ldcf, nullptr, nullptr, 0.f};
   return gemm_dispatch(tc::TEPI_STORE, A, lda, Bt, M, N, K, ea, st);
+}
+
+// [da | dv] = SwiGLU gate backward of [u | v] = X W1 (recomputed, W1 in TEPI_SWIGLU's interleaved Bt
+// layout [2 rd x d]) given dH [rows x rd]: da -> dag[:, 0:rd], dv -> dag[:, rd:2rd] (bf16, row stride lddag)
+cudaError_t tc_swiglu_bwd(const void *X, int64_t ldx, int64_t rows, const void *W1, int d, int rd, const void *dH,
+                          int64_t ldh, void *dag, int64_t lddag, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  tc::EpiArgs ea{(bf16 *)dag, lddag, nullptr, 0, nullptr, nullptr, 0.f, (const bf16 *)dH, ldh, rd};
+  return gemm_dispatch(tc::TEPI_SWIGLU_BWD, X, ldx, W1, rows, 2 * rd, d, ea, st);
 }
 
 // ---- SwiGLUFFN (+LN) over rows, as two tcgen05 GEMMs with H (bf16) in the caller's scratch ----
