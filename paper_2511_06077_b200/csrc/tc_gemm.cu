@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       static_assert(OUT_COLS >= 32 || EPI == TEPI_SWIGLU, "32-column output blocks");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(&acc_empty[a], 0));  // the leader may reuse accumulator a
+      if (lane == 0) mbar_arrive_cluster_relaxed(mapa_shared(&acc_empty[a], 0));  // the leader may reuse accumulator a
     }
   }
   tc_fence_before();

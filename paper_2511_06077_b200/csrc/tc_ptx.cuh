@@ -134,6 +134,13 @@ __device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *m
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// the same with relaxed semantics: orders only what tcgen05.fence::before_thread_sync orders (TMEM
+// reads of an accumulator before the peer's MMAs reuse it), not the thread's global stores -- the
+// release form compiles to MEMBAR.ALL.GPU + ERRBAR, a wait for every store in flight (17 % of the
+// GEMM epilogue's stall samples, profiles/r2_prof_gemm_epilogue)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t *slot, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
                : "memory");
