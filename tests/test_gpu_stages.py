@@ -185,3 +185,39 @@ def test_attention_stage_isolated(d, h, m, wq):
         e = rowrel(Yg, ref)
         assert e.max() <= 1e-2, (layer, e.max(), int(e.argmax()))
     mdl.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [8, 16])
+def test_attention_stage_isolated_many_items_per_cta(m):
+    """The persistent narrow kernel with several items per CTA (600 requests over <= 148 CTAs), many
+    of them one key tile long or a single key: the deferred per-item output (written during the next
+    item's first tile) and the O^T double buffer must hand every item its own sums and columns.
+    Same bound as test_attention_stage_isolated."""
+    import torch
+    import paper_2511_06077_b200 as stca
+    rng = np.random.default_rng(5)
+    lengths = rng.integers(1, 700, 600)
+    lengths[::7] = 1
+    lengths[3::11] = 128
+    cfg = make_cfg(B=len(lengths), m=m, d=128, h=4, M=2)
+    wl = workload.make_workload(cfg, seed=23, lengths=lengths)
+    c = wl.cfg
+    mdl = stca.STCA(workload.full_weights(wl), d=128, h=4, r=c.r, M=c.M, dtype="bf16")
+    X, xt = device_inputs(wl)
+    NQ = wl.Nt * 4
+    Ucap = torch.zeros(NQ, 128, dtype=torch.int16, device="cuda")
+    Ycap = torch.zeros(NQ, 128, dtype=torch.int16, device="cuda")
+    Z = torch.empty(wl.Nt, c.M, 128, device="cuda")
+    mdl.project_history(X, wl.hist_off)
+    mdl.debug_capture(2, Ucap, Ycap)
+    mdl.forward(xt, wl.tgt_off, Z, None)
+    torch.cuda.synchronize()
+    U = workload.bits_to_f32(Ucap.cpu().numpy().view(np.uint16)).reshape(NQ, 128).astype(np.float64)
+    Yg = workload.bits_to_f32(Ycap.cpu().numpy().view(np.uint16)).reshape(NQ, 128).astype(np.float64)
+    Xc = mdl.read_cache(2, 0, int(lengths.sum())).astype(np.float64)
+    ref, A = _f64_attention(U, Xc, lengths, wl.tgt_off, 4)
+    assert np.isfinite(Yg).all()
+    ratio = np.abs(Yg - ref) / (KC_BOUND * A + 1e-30)
+    assert ratio.max() <= 1.0, (ratio.max(), np.unravel_index(ratio.argmax(), ratio.shape))
+    mdl.close()
