@@ -29,6 +29,13 @@
 #ifndef STCA_NARROW_LAZY
 #define STCA_NARROW_LAZY 8.f  // rescale threshold in log2 units (a test build sets 0)
 #endif
+#ifndef STCA_NARROW_DEFER64
+#define STCA_NARROW_DEFER64 0
+#endif
+#ifndef STCA_NARROW_FMA_NUM  // fraction of a thread's exponentials on the FMA pipe (A/B builds: 3 / 8 measured
+#define STCA_NARROW_FMA_NUM 0  // 4 % slower at train and equal at multi -- MUFU does not bound this kernel,
+#define STCA_NARROW_FMA_DEN 8  // profiles/r2_narrow_fma_ab)
+#endif
 #ifndef STCA_NARROW_PF
 #define STCA_NARROW_PF 6  // key tiles prefetched into L2 ahead of the TMA loads (0: off)
 #endif
@@ -42,6 +49,7 @@ template <int NQ_>
 struct NCfg {
   static constexpr int D = 128, BK = 128, NQ = NQ_;   // d, keys per tile, query columns (64 or 32)
   static constexpr int CW = NQ / 4;                    // query columns per softmax warp (4 column groups)
+  static constexpr int NFMA = STCA_NARROW_FMA_NUM * CW / STCA_NARROW_FMA_DEN;  // of them, exponentials on the FMA pipe
   static constexpr int X_BYTES = BK * D * 2;           // 2 boxes of 128 keys x 64 d (16 KB each)
   // 5 stages: a tile holds its slot from the TMA issue until its PV completes (~2 slots busy with
   // S / softmax / PV), so the slots left in flight bound the HBM bytes in flight per SM; the L2
@@ -51,7 +59,16 @@ struct NCfg {
   static constexpr int U_BYTES = NQ * D * 2;           // U: 64 queries x 128 d, 2 boxes of 8 KB
   static constexpr int RED_BYTES = 4 * 4 * CW * 4;     // [column group][quarter][CW] column partials
   static constexpr int NSW = 16, THREADS = (NSW + 3) * 32;  // softmax warps; + producer, S / PV issuers
-  static constexpr int SMEM = 1024 + STAGES * X_BYTES + 2 * P_BYTES + 2 * U_BYTES + RED_BYTES + 64 + 256;
+  // DEFERRED epilogue (an item's output written during the next item's first tile): at 32 columns;
+  // at 64 the deferred item's state spills the tile loop (96 registers, measured slower: r2_narrow_defer)
+  static constexpr bool DEFER = NQ == 32 || STCA_NARROW_DEFER64;
+  // the deferred epilogue's copies of an item's column partial sums and reference maxima
+  static constexpr int DEF_BYTES = DEFER ? RED_BYTES + 4 * CW * 4 : 0;
+  static constexpr int USED = STAGES * X_BYTES + 2 * P_BYTES + 2 * U_BYTES + RED_BYTES + DEF_BYTES + 64 + 256;
+  // 1 KB to align the base up to 1024 when it fits; at NQ = 64 it does not (227 KB), and the kernel
+  // traps if the dynamic shared memory base is not 1024-aligned (it follows the 1 KB the system reserves)
+  static constexpr int RESERVE = USED + 1024 <= 232448 ? 1024 : 0;
+  static constexpr int SMEM = RESERVE + USED;
   static constexpr uint32_t TS = 0, TO = 128;          // S^T buffers at 0 / 64, O^T buffers at 128 / 192
 };
 
@@ -115,7 +132,10 @@ __global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
   uint8_t *sP = sX + C::STAGES * C::X_BYTES;
   uint8_t *sU = sP + 2 * C::P_BYTES;                                   // 2 buffers
   float *sRed = reinterpret_cast<float *>(sU + 2 * C::U_BYTES);        // [4][4][16]
-  uint32_t *sFlag = reinterpret_cast<uint32_t *>(sRed + 4 * 4 * CW);   // [tile parity][column group]: 4 byte flags
+  float *sDefL = sRed + 4 * 4 * CW;                                    // [4][4][CW] deferred item's partial sums
+  float *sDefM = sDefL + 4 * 4 * CW;                                   // [4][CW] deferred item's maxima
+  // (both only with C::DEFER: DEF_BYTES is 0 otherwise)
+  uint32_t *sFlag = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(sRed) + C::RED_BYTES + C::DEF_BYTES);
   uint64_t *bar = reinterpret_cast<uint64_t *>(sFlag + 16);
   uint64_t *u_full = bar;                      // 2 (TMA)
   uint64_t *u_free = u_full + 2;               // 2 (S issuer commit after an item's last S)
@@ -130,6 +150,7 @@ __global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int i0 = cta_off[blockIdx.x], i1 = cta_off[blockIdx.x + 1];
+  if (C::RESERVE == 0 && (smem_u32(smem_raw) & 1023) != 0) __trap();  // no room to align (see NCfg)
 
   if (warp == C::NSW && lane == 0) {
     tma_prefetch(&mapX);
@@ -265,6 +286,41 @@ __global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
     const int key = q * 32 + lane;           // S^T lane = key within the tile; O^T lane = d
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
     int g = 0;
+    // DEFERRED epilogue: an item's output is written during the NEXT item's first tile (after its P is
+    // handed to the PV issuer), so the softmax warps neither wait for the item's last PV nor hold up the
+    // next item's pipeline start; the item's partial sums / maxima wait in sDefL / sDefM
+    bool dpend = false;
+    int dob = 0, dg = 0;  // deferred item's O^T buffer and last global tile
+    AttnItem dit{};
+    auto deferred_epilogue = [&]() {
+      mbar_wait(&pv_done[dg & 1], (dg >> 1) & 1);  // the deferred item's last PV
+      tc_fence_after();
+      uint32_t o[CW];
+      tmem_ldn<CW>(tmem + lanes + C::TO + dob * C::NQ + CW * cg, o);  // thread = output column d, CW queries
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[dob]);  // the PV issuer may start item + 2 in this buffer
+      const int d = key;
+#pragma unroll
+      for (int e = 0; e < CW; ++e) {
+        const int qn = CW * cg + e;
+        if (qn < dit.nq) {
+          const float ln = sDefL[(cg * 4) * CW + e] + sDefL[(cg * 4 + 1) * CW + e] + sDefL[(cg * 4 + 2) * CW + e] +
+                           sDefL[(cg * 4 + 3) * CW + e];
+          const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
+          if (dit.part_row < 0) {
+            if constexpr (STD) Y[((dit.qrow0 + qn) * yh + dit.pad) * C::D + d] = y;
+            else Y[(dit.qrow0 + qn) * C::D + d] = y;
+          } else {  // partials hold the chunk's normalised output O / l, then (m, l)
+            uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (dit.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
+            reinterpret_cast<bf16 *>(pr)[d] = y;
+            if (d == 0) *reinterpret_cast<float2 *>(pr + 2 * C::D) = make_float2(sDefM[cg * CW + e], ln);
+          }
+        }
+      }
+      dpend = false;
+    };
     for (int n = i0; n < i1; ++n) {
       const AttnItem it = items[cta_items[n]];
       const int ni = n - i0, ob = ni & 1, nt = (it.klen + C::BK - 1) / C::BK;
@@ -333,11 +389,21 @@ __global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
             tmem_st_wait();
           }
         }
+        // the exponentials on MUFU; an A/B build puts the first C::NFMA of the thread's CW on the FMA pipe
+        // (packed cubic, ex2_fma2, relative error 1e-4)
         uint32_t w[CW / 2];
 #pragma unroll
         for (int i = 0; i < CW / 2; ++i) {
-          const float p0 = kv ? ex2(__uint_as_float(sr[2 * i]) - mref[2 * i]) : 0.f;
-          const float p1 = kv ? ex2(__uint_as_float(sr[2 * i + 1]) - mref[2 * i + 1]) : 0.f;
+          const float x0 = __uint_as_float(sr[2 * i]) - mref[2 * i], x1 = __uint_as_float(sr[2 * i + 1]) - mref[2 * i + 1];
+          float p0, p1;
+          if (2 * i < C::NFMA) {
+            const uint64_t e2 = ex2_fma2(f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f)));
+            p0 = kv ? f2_lo(e2) : 0.f;
+            p1 = kv ? f2_hi(e2) : 0.f;
+          } else {
+            p0 = kv ? ex2(x0) : 0.f;
+            p1 = kv ? ex2(x1) : 0.f;
+          }
           l[2 * i] += p0;
           l[2 * i + 1] += p1;
           w[i] = pack_bf16(p0, p1);
@@ -352,41 +418,66 @@ __global__ void __launch_bounds__(NCfg<NQ>::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b]);
+        if (C::DEFER && dpend) deferred_epilogue();  // the previous item's output (first tile of this item only)
       }
-      // ---- sums over the keys: per warp by recursive halving, then the 4 lane quarters through SMEM ----
-      named_bar_sync(1 + cg, 128);  // the last tile's sRed reads are done
-      {
-        const float red = xreduce<false, CW>(l, lane);
-        if (lane < CW) sRed[(cg * 4 + q) * CW + lane] = red;
-      }
-      if (nt >= 1) mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);  // the item's last PV
-      tc_fence_before();
-      named_bar_sync(1 + cg, 128);
-      tc_fence_after();
-      uint32_t o[CW];
-      tmem_ldn<CW>(tmem + lanes + C::TO + ob * C::NQ + CW * cg, o);  // thread = output column d, CW queries
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[ob]);  // the PV issuer may start item ni + 2 in this buffer
-      const int d = key;
+      if constexpr (C::DEFER) {
+        // ---- sums over the keys: per warp by recursive halving; the 4 lane quarters are added by the
+        // deferred epilogue (sDefL survives this item's successor's first tile, which reuses sRed) ----
+        if (nt == 1) named_bar_sync(1 + cg, 128);  // the deferred epilogue in this (only) tile read sDefL
+        {
+          const float red = xreduce<false, CW>(l, lane);
+          if (lane < CW) sDefL[(cg * 4 + q) * CW + lane] = red;
+          if (q == 0 && lane < CW) {
+            float mv = mref[0];
 #pragma unroll
-      for (int e = 0; e < CW; ++e) {
-        const int qn = CW * cg + e;
-        if (qn < it.nq) {
-          const float ln = sRed[(cg * 4) * CW + e] + sRed[(cg * 4 + 1) * CW + e] + sRed[(cg * 4 + 2) * CW + e] +
-                           sRed[(cg * 4 + 3) * CW + e];
-          const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
-          if (it.part_row < 0) {
-            if constexpr (STD) Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
-            else Y[(it.qrow0 + qn) * C::D + d] = y;
-          } else {  // partials hold the chunk's normalised output O / l, then (m, l)
-            uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
-            reinterpret_cast<bf16 *>(pr)[d] = y;
-            if (d == 0) *reinterpret_cast<float2 *>(pr + 2 * C::D) = make_float2(mref[e], ln);
+            for (int c = 1; c < CW; ++c) mv = lane == c ? mref[c] : mv;
+            sDefM[cg * CW + lane] = mv;
+          }
+        }
+        dpend = true;
+        dob = ob;
+        dg = g - 1;
+        dit = it;
+      } else {
+        // ---- sums over the keys: per warp by recursive halving, then the 4 lane quarters through SMEM ----
+        named_bar_sync(1 + cg, 128);  // the last tile's sRed reads are done
+        {
+          const float red = xreduce<false, CW>(l, lane);
+          if (lane < CW) sRed[(cg * 4 + q) * CW + lane] = red;
+        }
+        if (nt >= 1) mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);  // the item's last PV
+        tc_fence_before();
+        named_bar_sync(1 + cg, 128);
+        tc_fence_after();
+        uint32_t o[CW];
+        tmem_ldn<CW>(tmem + lanes + C::TO + ob * C::NQ + CW * cg, o);  // thread = output column d, CW queries
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_free[ob]);  // the PV issuer may start item ni + 2 in this buffer
+        const int d = key;
+#pragma unroll
+        for (int e = 0; e < CW; ++e) {
+          const int qn = CW * cg + e;
+          if (qn < it.nq) {
+            const float ln = sRed[(cg * 4) * CW + e] + sRed[(cg * 4 + 1) * CW + e] + sRed[(cg * 4 + 2) * CW + e] +
+                             sRed[(cg * 4 + 3) * CW + e];
+            const bf16 y = __float2bfloat16(__uint_as_float(o[e]) / ln);
+            if (it.part_row < 0) {
+              if constexpr (STD) Y[((it.qrow0 + qn) * yh + it.pad) * C::D + d] = y;
+              else Y[(it.qrow0 + qn) * C::D + d] = y;
+            } else {  // partials hold the chunk's normalised output O / l, then (m, l)
+              uint8_t *pr = reinterpret_cast<uint8_t *>(part) + (it.part_row + qn) * (int64_t)part_row_bytes(C::D, 2);
+              reinterpret_cast<bf16 *>(pr)[d] = y;
+              if (d == 0) *reinterpret_cast<float2 *>(pr + 2 * C::D) = make_float2(mref[e], ln);
+            }
           }
         }
       }
+    }
+    if (C::DEFER && dpend) {  // the CTA's last item
+      named_bar_sync(1 + cg, 128);  // its sDefL / sDefM writes are visible to the column group
+      deferred_epilogue();
     }
   }
   tc_fence_before();
