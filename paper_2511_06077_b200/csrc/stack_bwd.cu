@@ -153,6 +153,11 @@ cudaError_t stack_bwd(void **blas, const StackBwd &a, cudaStream_t st) {
   }
   cublasHandle_t hb = (cublasHandle_t)*blas;
   if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  // the target side's fp32 GEMMs on the tensor cores in TF32 (10-bit mantissa products, fp32 accumulation:
+  // finer than the bf16 operands the forward's target side uses); as SIMT SGEMMs they were ~10 % of the
+  // training step (profiles/r2_final3_launches_stack_bwd.csv).  The history path's GEMMs (bf16 operands)
+  // are not affected by the math mode.
+  if (cublasSetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   const int d = a.d, h = a.h, rd = a.rd, M = a.M, dh = d / h;
   const int64_t Nt = a.Nt, NQ = Nt * h, ldo = (int64_t)(M + 1) * d;
   const int nt = (int)Nt;
