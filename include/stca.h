@@ -281,8 +281,10 @@ stca_status stca_attention_backward(stca_handle *h, int32_t layer, const void *U
  * (DEVICE fp32 [rows x d], e.g. from stca_attention_backward), ACCUMULATES dX += dLoss/dX (DEVICE fp32
  * [rows x d]; sum over the layers by calling once per layer) and WRITES the layer's weight gradients
  * dWu, dWv [d x rd], dWo [rd x d], dgamma, dbeta [d] (DEVICE fp32, the weights' [in x out] orientation).
- * The forward is recomputed (no activations are kept); the GEMMs run on cuBLAS (bf16 operands, fp32
- * accumulation), SwiGLU and LayerNorm backward on kernels of the library.  Each history row appears once
+ * The forward is recomputed (no activations are kept) on the library's tcgen05 GEMMs (the SwiGLU in the
+ * epilogue), the SwiGLU-gate backward runs in the epilogue of a tcgen05 GEMM that recomputes X [Wu | Wv],
+ * the LayerNorm backward on a kernel of the library, dH / dX / the weight gradients on cuBLAS (bf16
+ * operands, fp32 accumulation).  Each history row appears once
  * per request however many targets share it: the gradients are aggregated at the request level.
  * Asynchronous on `stream`.  STATE without a projection, SHAPE for a row-count mismatch, UNSUPPORTED off
  * the bf16 path or over a session cache. */
@@ -305,7 +307,7 @@ stca_status stca_history_backward(stca_handle *h, int32_t layer, const void *X, 
  *   - dX (DEVICE fp32 [rows x d] or NULL): d loss / d X over the rows the projection kept, in cache order
  *     (X: DEVICE bf16, those rows, as stca_history_backward; rows must equal the cache's row count);
  *   - dxt (DEVICE fp32 [N_t x d] or NULL): d loss / d x_t.
- * Per layer, from the last: target-side GEMMs of Eq.(6)-(7) in fp32 (cuBLAS), the attention backward
+ * Per layer, from the last: target-side GEMMs of Eq.(6)-(7) (cuBLAS, fp32 storage, TF32 tensor cores), the attention backward
  * (tcgen05 kernel, dX~ summed over the request's target-head rows inside the MMA), the history path's
  * LN + SwiGLU-FFN backward (stca_history_backward's kernels).  Asynchronous on `stream`.  STATE without a
  * projection or for a B mismatch; UNSUPPORTED off the bf16 d = 128 path, in split-history mode or over a

@@ -5,20 +5,23 @@
 // per request, S = U_b X~_b^T, P = 2^(S - m), Y = P X~_b / sum, U pre-scaled by log2(e)/sqrt(d_h).
 // With 8 targets x 4 heads = 32 query rows per request (the multi config) a 128-row query tile
 // wastes 3/4 of every MMA and of the softmax, and the kernel stops being HBM-bound.  Here the keys
-// are the MMA's M dimension and the queries its N dimension (N = 64):
-//   S^T [128 keys x 64 queries]  = X~_tile (SMEM, K-major A) . U^T (SMEM, K-major B)
-//   O^T [128 d    x 64 queries] += X~_tile^T (the SAME SMEM tile as an MN-major A) . P^T (SMEM, MN-major B)
-// so the MMA work per key tile is 128x64x128 twice (not 128x128x128 twice) and a CTA streams X~ at
-// HBM speed.  TMEM: S^T double buffer (2 x 64 columns) | O^T double buffer (2 x 64 columns).
+// are the MMA's M dimension and the queries its N dimension (N = NQ = 64, or 32 for requests with
+// m_b h <= 32: a second instantiation chosen per request, P^T then in a SWIZZLE_64B layout):
+//   S^T [128 keys x NQ queries]  = X~_tile (SMEM, K-major A) . U^T (SMEM, K-major B)
+//   O^T [128 d    x NQ queries] += X~_tile^T (the SAME SMEM tile as an MN-major A) . P^T (SMEM, MN-major B)
+// so the MMA work per key tile is 128 x NQ x 128 twice (not 128x128x128 twice) and a CTA streams X~ at
+// HBM speed.  TMEM: S^T double buffer (2 x NQ columns) | O^T double buffer (2 x NQ columns).
 //
-// Softmax along TMEM lanes: a thread owns one key (lane) and 16 query columns (four warps per
-// lane quarter; with 8 warps of 32 columns the per-tile latency chain left the tile at ~2400 cycles).  A query's running maximum is LAZY (as in tc_attn_wide.cu): a key tile only triggers the
-// column-max reduction (16 shuffles per warp by recursive halving + 4 partials through SMEM) when
+// Softmax along TMEM lanes: a thread owns one key (lane) and NQ/4 query columns (four warps per
+// lane quarter; with 8 warps of 32 columns the per-tile latency chain left the tile at ~2400 cycles).
+// A query's running maximum is LAZY (as in tc_attn_wide.cu): a key tile only triggers the
+// column-max reduction (recursive-halving shuffles per warp + 4 partials through SMEM) when
 // some score exceeds the reference maximum by more than 2^8, which after the first tile is rare;
 // then the affected O^T columns and sums are rescaled in place after the PVs so far completed.
-// Sums stay per thread (per key, per query) until one reduction at the end.
+// Sums stay per thread (per key, per query) until one reduction at the end of the item; at NQ = 32
+// the item's output is written during the NEXT item's first tile (deferred epilogue, NCfg::DEFER).
 //
-// Warp roles (608 threads): 0..15 softmax (warp w: keys 32(w&3).., queries 16(w>>2)..) and output,
+// Warp roles (608 threads): 0..15 softmax (warp w: keys 32(w&3).., queries NQ/4 (w>>2)..) and output,
 // 16 TMA producer, 17 TMEM allocator + S issuer, 18 PV issuer.  Persistent: one CTA per SM.
 #include <math.h>
 
