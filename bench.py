@@ -560,9 +560,11 @@ def main():
                                               alg["proj_bytes"], prof["project"][0] / prof["project"][1], pk,
                                               peak_kind, c.name))
             if prof["attention"][1]:
+                # the committed ncu summaries are captures of the reordered form: no attention entry for another
                 kernels.append(roofline_entry("ragged single-query attention (a4, one layer)", "attention",
                                               alg["attn_flops_layer"], alg["attn_bytes_layer"],
-                                              prof["attention"][0] / prof["attention"][1], pk, peak_kind, c.name))
+                                              prof["attention"][0] / prof["attention"][1], pk, peak_kind,
+                                              c.name if args.form == "reordered" else f"{c.name}/{args.form}"))
             for k in kernels:
                 k["timing"] = ("CUDA events on the launching stream around the launch, K steps after the timed "
                                "region (an upper bound of the kernel time: the events also hold its launch and "
